@@ -1,0 +1,161 @@
+/*
+ * lfsr_b200 -- C ABI of the B200-native A5/1 state-graph kernels (arXiv 1210.6411,
+ * steps 1-3).  Plain pointers and sizes only; no torch types cross this boundary.
+ *
+ * The reference (`lfsrcycles`, /root/reference/pkg/src/lfsrcycles) is pure Python and
+ * has no FFI of its own; each entry point below replaces one reference function (the
+ * "operator API" of SURVEY.md §8(b)) and says which.  INTEGRATION.md shows the ctypes
+ * binding the Python package uses (paper_1210_6411_b200/_native.py).
+ *
+ * Conventions
+ *  - States are packed u64 exactly as cipher.py:90-131 (R1 low bits, R3 high bits).
+ *  - Functions without a `_device` suffix take HOST buffers, are synchronous, and do
+ *    the host<->device copies themselves.  `_device` variants take device pointers and
+ *    a cudaStream_t (passed as void*), enqueue work and return without synchronising.
+ *  - Return 0 on success or a negative LC_ERR_* code; lc_last_error() (thread-local)
+ *    holds the message.  No C++ exception crosses the ABI.
+ *  - Only the three built-in ciphers (A5/1, mini567, mini789 -- cipher.py:173-194) have
+ *    compiled kernels; any other spec returns LC_ERR_UNSUPPORTED (there is no CPU path).
+ */
+#ifndef LFSR_B200_H
+#define LFSR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LC_ABI_VERSION 1
+
+#define LC_OK 0
+#define LC_ERR_ARG (-1)          /* ValueError in the reference (bitslice.py:269-272, ...) */
+#define LC_ERR_CUDA (-2)         /* CUDA runtime failure */
+#define LC_ERR_UNSUPPORTED (-3)  /* spec without a compiled kernel */
+#define LC_ERR_CAP (-4)          /* StrideError: walk cap exceeded (bitslice.py:316-322) */
+#define LC_ERR_INVALID_STATE (-5)/* a start has a zero register; the reference
+                                    walks it to the cap and raises StrideError */
+#define LC_ERR_OVERFLOW (-6)     /* output capacity too small */
+
+/* Cipher instance (cipher.py:57-170 CipherSpec): register lengths, feedback tap masks
+ * (bit i set = tap at register bit i) and clock tap positions. */
+typedef struct {
+    int32_t lengths[3];
+    uint64_t tap_masks[3];
+    int32_t clock_taps[3];
+} lc_spec;
+
+/* Layout of the u64 statistics block every walk accumulates into (device or host).
+ * All counters are integers (bit-exact, order independent) and are summed / min-ed /
+ * max-ed across ranks by the distributed driver (NCCL all-reduce). */
+enum {
+    LC_ST_EDGES = 0,        /* walks (legs) completed                          (sum) */
+    LC_ST_TRANSITIONS = 1,  /* sum of dist = A5/1 transitions walked           (sum) */
+    LC_ST_MIN = 2,          /* min dist                                         (min) */
+    LC_ST_MAX = 3,          /* max dist                                         (max) */
+    LC_ST_SQ_LO = 4,        /* sum (dist - hist_lo)^2, low 64 bits              (u128 sum) */
+    LC_ST_SQ_HI = 5,        /*                         high 64 bits                      */
+    LC_ST_ERROR = 6,        /* 0 or -LC_ERR_* of the first error                        */
+    LC_ST_ERROR_INDEX = 7,  /* smallest start index that raised (min)                   */
+    LC_ST_HIST_LO = 8,      /* histogram: bin b counts dist in [lo + b<<shift, ...)      */
+    LC_ST_HIST_SHIFT = 9,
+    LC_ST_HIST_BINS = 10,   /* number of interior bins; +2 under/overflow bins          */
+    LC_ST_LAUNCHES = 11,    /* kernels launched by the call (host-side count)           */
+    LC_ST_HEADER = 16       /* histogram starts here: [under, bins..., over]            */
+};
+
+typedef struct lc_ctx lc_ctx;
+
+int lc_abi_version(void);
+const char *lc_last_error(void);
+int lc_device_count(int *count);
+
+/* One context per (device, host thread).  Owns scratch buffers and a stream. */
+int lc_ctx_create(int device, lc_ctx **out);
+int lc_ctx_destroy(lc_ctx *ctx);
+int lc_ctx_sm_count(lc_ctx *ctx, int *sms);
+int lc_ctx_synchronize(lc_ctx *ctx);
+
+/* Pinned host memory for the end-to-end (host-buffer) path. */
+int lc_host_alloc(uint64_t bytes, void **out);
+int lc_host_free(void *p);
+
+/* Roofline denominator (no reference counterpart): measured sustained 32-bit LOP3
+ * results/s of the whole device and the SM clock seen meanwhile (MHz). */
+int lc_lop3_peak(lc_ctx *ctx, double *lop3_per_s, double *sm_mhz);
+
+/* Kernel launches made by this thread's lc_* calls since the last reset. */
+uint64_t lc_launch_count(void);
+void lc_launch_count_reset(void);
+
+/* ---------------------------------------------------------------- step 3: walks */
+
+/* Replaces bitslice._run_walks (bitslice.py:259-323), i.e. forward_to_candidate
+ * (bitslice.py:326-342, legs = 1) and candidate_hops (bitslice.py:345-354, stride = 1,
+ * legs >= 1).  For every start, `legs` consecutive candidate hops; hop 1 is the first
+ * candidate at clock >= max(stride, 1).  dest/dist are [n][legs] row-major.
+ * max_clocks: the reference cap (bitslice.py:273-274); StrideError semantics in
+ * DESIGN.md §"Cap".  refill: 0 = auto, 1 = refill a lane as soon as it finishes,
+ * 1024 = refill a warp only when all its 1024 lanes are idle (near-constant walks).
+ * hist_lo/hist_shift/hist_bins configure the chain-length histogram in `stats`
+ * (LC_ST_HEADER + hist_bins + 2 words). */
+int lc_walk(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3, const uint64_t *starts,
+            uint64_t n, uint64_t stride, uint64_t max_clocks, uint32_t legs, uint32_t refill,
+            uint64_t *dest, uint64_t *dist, uint64_t hist_lo, uint32_t hist_shift,
+            uint32_t hist_bins, uint64_t *stats);
+int lc_walk_device(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3,
+                   const uint64_t *d_starts, uint64_t n, uint64_t stride, uint64_t max_clocks,
+                   uint32_t legs, uint32_t refill, uint64_t *d_dest, uint64_t *d_dist,
+                   uint64_t hist_lo, uint32_t hist_shift, uint32_t hist_bins,
+                   uint64_t *d_stats, void *stream);
+
+/* Replaces bitslice.clock_sliced (bitslice.py:223-228): every state advanced t clocks. */
+int lc_clock(lc_ctx *ctx, const lc_spec *spec, const uint64_t *xs, uint64_t n, uint64_t t,
+             uint64_t *out);
+
+/* ------------------------------------------------------- steps 1-2: predicate, prune */
+
+/* Replaces is_candidate (cipher.py:420-428) over a batch: out[i] = 1 iff xs[i] is a
+ * special node (R3 == fixed, R3 leaves fixed on the next clock, has a predecessor). */
+int lc_is_candidate(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3, const uint64_t *xs,
+                    uint64_t n, uint8_t *out);
+
+/* Replaces predecessors (cipher.py:342-369) over a batch: out is [n][4] in the
+ * reference's LUT pattern order, count[i] in 0..4 (the leaf filter is count == 0). */
+int lc_predecessors(lc_ctx *ctx, const lc_spec *spec, const uint64_t *xs, uint64_t n,
+                    uint64_t *out, uint8_t *count);
+
+/* Replaces enumerate_candidates (pipeline.py:104-118) restricted to R2 rows
+ * [r2_lo, r2_hi): every candidate, ascending.  Writes min(count, cap) states and
+ * sets *count; returns LC_ERR_OVERFLOW if count > cap. */
+int lc_enumerate(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3, uint64_t r2_lo,
+                 uint64_t r2_hi, uint64_t *out, uint64_t cap, uint64_t *count);
+int lc_enumerate_device(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3, uint64_t r2_lo,
+                        uint64_t r2_hi, uint64_t *d_out, uint64_t cap, uint64_t *d_count,
+                        void *stream);
+
+/* Replaces the per-candidate decision of prune_shallow_segments (pipeline.py:163-222):
+ * mode 0 = dfs (_dfs_is_shallow, depth limit), 1 = bfs (_bfs_is_small, node limit).
+ * removed[i] = 1 iff cands[i] roots a shallow segment; work[i] = the reference's
+ * per-candidate `expanded` counter (LIFO order replicated). */
+int lc_prune(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3, int32_t mode, uint64_t limit,
+             const uint64_t *cands, uint64_t n, uint8_t *removed, uint64_t *work);
+
+/* Seeded synthetic start set (K0): the first n special nodes of the
+ * counter-based stream trial i -> (r1, r2) = split(splitmix64(seed + i*golden)), in trial
+ * order.  *trials_used = trials consumed.  Host and device variants. */
+int lc_random_candidates(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3, uint64_t seed,
+                         uint64_t n, uint64_t *out, uint64_t *trials_used);
+int lc_random_candidates_device(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3,
+                                uint64_t seed, uint64_t n, uint64_t *d_out, void *stream);
+
+/* Closure check of build_skeleton_edges (pipeline.py:251-255): first i with
+ * queries[i] not in the ascending array `sorted_set`, or n if all are members. */
+int lc_first_missing(lc_ctx *ctx, const uint64_t *sorted_set, uint64_t m, const uint64_t *queries,
+                     uint64_t n, uint64_t *first_missing);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LFSR_B200_H */

@@ -1,0 +1,501 @@
+// C ABI (include/lfsr_b200.h): contexts, scratch management, spec dispatch, host-buffer
+// wrappers.  The kernels live in walk.cu / kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "lfsr_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local uint64_t g_launches = 0;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define LC_CUDA(expr)                                                                      \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess) return fail(LC_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+lc::SpecId identify(const lc_spec* s) {
+  if (!s) return lc::SpecId::UNSUPPORTED;
+  struct Known {
+    int l[3];
+    uint64_t t[3];
+    int c[3];
+    lc::SpecId id;
+  };
+  static const Known known[] = {
+      {{19, 22, 23},
+       {(1ull << 13) | (1ull << 16) | (1ull << 17) | (1ull << 18), (1ull << 20) | (1ull << 21),
+        (1ull << 7) | (1ull << 20) | (1ull << 21) | (1ull << 22)},
+       {8, 10, 10},
+       lc::SpecId::A51},
+      {{5, 6, 7}, {(1ull << 1) | (1ull << 4), (1ull << 4) | (1ull << 5), (1ull << 5) | (1ull << 6)}, {2, 2, 3}, lc::SpecId::MINI567},
+      {{7, 8, 9},
+       {(1ull << 5) | (1ull << 6), (1ull << 3) | (1ull << 4) | (1ull << 5) | (1ull << 7), (1ull << 3) | (1ull << 8)},
+       {3, 3, 4},
+       lc::SpecId::MINI789},
+  };
+  for (const Known& k : known) {
+    bool eq = true;
+    for (int i = 0; i < 3; ++i)
+      eq = eq && s->lengths[i] == k.l[i] && s->tap_masks[i] == k.t[i] && s->clock_taps[i] == k.c[i];
+    if (eq) return k.id;
+  }
+  return lc::SpecId::UNSUPPORTED;
+}
+
+uint32_t default_fixed(lc::SpecId id) {
+  switch (id) {
+    case lc::SpecId::A51: return 0x2AAA00u;
+    case lc::SpecId::MINI567: return 0x22u;
+    case lc::SpecId::MINI789: return 0xaau;
+    default: return 0u;
+  }
+}
+
+int l3_of(lc::SpecId id) { return id == lc::SpecId::A51 ? 23 : (id == lc::SpecId::MINI567 ? 7 : 9); }
+
+int check_spec(const lc_spec* spec, lc::SpecId* id) {
+  *id = identify(spec);
+  if (*id == lc::SpecId::UNSUPPORTED)
+    return fail(LC_ERR_UNSUPPORTED,
+                "no compiled kernel for this cipher spec (built-ins: a51, mini567, mini789)");
+  return LC_OK;
+}
+
+int check_fixed(lc::SpecId id, uint64_t fixed_r3) {
+  const int l3 = l3_of(id);
+  if (fixed_r3 == 0 || fixed_r3 >= (1ull << l3))
+    return fail(LC_ERR_ARG, "fixed R3 value must be a nonzero %d-bit value", l3);
+  return LC_OK;
+}
+
+}  // namespace
+
+struct lc_ctx {
+  int device = 0;
+  int sms = 0;
+  cudaStream_t stream = nullptr;
+  DevBuf meta, queue, stats, a, b, c, d, scratch;
+};
+
+extern "C" {
+
+int lc_abi_version(void) { return LC_ABI_VERSION; }
+
+const char* lc_last_error(void) { return g_err.c_str(); }
+
+uint64_t lc_launch_count(void) { return g_launches; }
+void lc_launch_count_reset(void) { g_launches = 0; }
+
+int lc_device_count(int* count) {
+  LC_CUDA(cudaGetDeviceCount(count));
+  return LC_OK;
+}
+
+int lc_ctx_create(int device, lc_ctx** out) {
+  if (!out) return fail(LC_ERR_ARG, "null output");
+  int n = 0;
+  LC_CUDA(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail(LC_ERR_ARG, "device %d out of range (%d devices)", device, n);
+  LC_CUDA(cudaSetDevice(device));
+  lc_ctx* c = new lc_ctx();
+  c->device = device;
+  cudaError_t e = cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(LC_ERR_CUDA, "context: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return LC_OK;
+}
+
+int lc_ctx_destroy(lc_ctx* ctx) {
+  if (!ctx) return LC_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (DevBuf* b : {&ctx->meta, &ctx->queue, &ctx->stats, &ctx->a, &ctx->b, &ctx->c, &ctx->d, &ctx->scratch})
+    b->release();
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return LC_OK;
+}
+
+int lc_ctx_sm_count(lc_ctx* ctx, int* sms) {
+  if (!ctx || !sms) return fail(LC_ERR_ARG, "null argument");
+  *sms = ctx->sms;
+  return LC_OK;
+}
+
+int lc_ctx_synchronize(lc_ctx* ctx) {
+  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  LC_CUDA(cudaSetDevice(ctx->device));
+  LC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LC_OK;
+}
+
+int lc_lop3_peak(lc_ctx* ctx, double* lop3_per_s, double* sm_mhz) {
+  if (!ctx || !lop3_per_s || !sm_mhz) return fail(LC_ERR_ARG, "null argument");
+  LC_CUDA(cudaSetDevice(ctx->device));
+  LC_CUDA(lc::measure_lop3_peak(ctx->sms, lop3_per_s, sm_mhz));
+  return LC_OK;
+}
+
+int lc_host_alloc(uint64_t bytes, void** out) {
+  if (!out) return fail(LC_ERR_ARG, "null output");
+  LC_CUDA(cudaMallocHost(out, bytes ? bytes : 1));
+  return LC_OK;
+}
+
+int lc_host_free(void* p) {
+  if (p) LC_CUDA(cudaFreeHost(p));
+  return LC_OK;
+}
+
+// ------------------------------------------------------------------------- walks
+
+int lc_walk_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const uint64_t* d_starts,
+                   uint64_t n, uint64_t stride, uint64_t max_clocks, uint32_t legs, uint32_t refill,
+                   uint64_t* d_dest, uint64_t* d_dist, uint64_t hist_lo, uint32_t hist_shift,
+                   uint32_t hist_bins, uint64_t* d_stats, void* stream) {
+  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  lc::SpecId id;
+  int rc = check_spec(spec, &id);
+  if (rc) return rc;
+  if ((rc = check_fixed(id, fixed_r3))) return rc;
+  if (stride < 1) return fail(LC_ERR_ARG, "stride must be >= 1");
+  if (legs < 1) return fail(LC_ERR_ARG, "legs must be >= 1");
+  if (hist_shift > 63) return fail(LC_ERR_ARG, "hist_shift must be < 64");
+  if (refill > 1024) return fail(LC_ERR_ARG, "refill must be in [0, 1024]");
+  if (!d_stats) return fail(LC_ERR_ARG, "stats buffer required");
+  LC_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+
+  // stats header: counters zero, min = ~0, error index = ~0, histogram config
+  LC_CUDA(lc::launch_init_stats(d_stats, hist_lo, hist_shift, hist_bins, st));
+  g_launches += 1;
+  if (n == 0) return LC_OK;
+  if (!d_starts || !d_dest || !d_dist) return fail(LC_ERR_ARG, "null buffer");
+
+  const bool static_f = fixed_r3 == default_fixed(id);
+  const int per_sm = lc::walk_blocks_per_sm(id, static_f);
+  const uint64_t lanes_per_block = lc::kWalkThreads * 32ull;
+  const uint64_t max_blocks = static_cast<uint64_t>(per_sm) * ctx->sms;
+  const uint64_t want = (n + lanes_per_block - 1) / lanes_per_block;
+  const int blocks = static_cast<int>(std::max<uint64_t>(1, std::min(max_blocks, want)));
+  uint32_t refill_min = refill;
+  if (refill_min == 0) refill_min = (legs == 1 && stride > 1) ? 1024u : 1u;
+
+  LC_CUDA(ctx->meta.ensure(static_cast<size_t>(blocks) * lanes_per_block * sizeof(lc::LaneMeta)));
+  LC_CUDA(ctx->queue.ensure(sizeof(unsigned long long)));
+  LC_CUDA(cudaMemsetAsync(ctx->queue.p, 0, sizeof(unsigned long long), st));
+
+  lc::WalkParams p{};
+  p.starts = d_starts;
+  p.n = n;
+  p.dst = d_dest;
+  p.dist = d_dist;
+  p.stride = stride;
+  p.cap1 = max_clocks == ~0ull ? ~0ull : max_clocks + 1;
+  p.hist_lo = hist_lo;
+  p.hist_shift = hist_shift;
+  p.hist_bins = hist_bins;
+  p.legs = legs;
+  p.fixed_r3 = static_cast<uint32_t>(fixed_r3);
+  p.refill_min = refill_min;
+  p.queue = ctx->queue.as<unsigned long long>();
+  p.stats = reinterpret_cast<unsigned long long*>(d_stats);
+  p.meta = ctx->meta.as<lc::LaneMeta>();
+  LC_CUDA(lc::launch_walk(id, static_f, p, blocks, st));
+  g_launches += 1;
+  return LC_OK;
+}
+
+int lc_walk(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const uint64_t* starts, uint64_t n,
+            uint64_t stride, uint64_t max_clocks, uint32_t legs, uint32_t refill, uint64_t* dest,
+            uint64_t* dist, uint64_t hist_lo, uint32_t hist_shift, uint32_t hist_bins,
+            uint64_t* stats) {
+  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  if (!stats) return fail(LC_ERR_ARG, "stats buffer required");
+  LC_CUDA(cudaSetDevice(ctx->device));
+  const size_t sb = (LC_ST_HEADER + hist_bins + 2ull) * sizeof(uint64_t);
+  const size_t nb = static_cast<size_t>(n) * sizeof(uint64_t);
+  const size_t ob = nb * std::max<uint32_t>(legs, 1);
+  LC_CUDA(ctx->a.ensure(std::max<size_t>(nb, 8)));
+  LC_CUDA(ctx->b.ensure(std::max<size_t>(ob, 8)));
+  LC_CUDA(ctx->c.ensure(std::max<size_t>(ob, 8)));
+  LC_CUDA(ctx->stats.ensure(sb));
+  if (n) LC_CUDA(cudaMemcpyAsync(ctx->a.p, starts, nb, cudaMemcpyHostToDevice, ctx->stream));
+  int rc = lc_walk_device(ctx, spec, fixed_r3, ctx->a.as<uint64_t>(), n, stride, max_clocks, legs, refill,
+                          ctx->b.as<uint64_t>(), ctx->c.as<uint64_t>(), hist_lo, hist_shift, hist_bins,
+                          ctx->stats.as<uint64_t>(), ctx->stream);
+  if (rc) return rc;
+  LC_CUDA(cudaMemcpyAsync(stats, ctx->stats.p, sb, cudaMemcpyDeviceToHost, ctx->stream));
+  LC_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (stats[LC_ST_ERROR]) {
+    const int code = -static_cast<int>(stats[LC_ST_ERROR]);
+    if (code == LC_ERR_CAP)
+      return fail(LC_ERR_CAP, "no candidate within %llu clocks; check the fixed R3 / stride configuration (start %llu)",
+                  static_cast<unsigned long long>(max_clocks), static_cast<unsigned long long>(stats[LC_ST_ERROR_INDEX]));
+    return fail(code, "start %llu has a zero register (invalid state)",
+                static_cast<unsigned long long>(stats[LC_ST_ERROR_INDEX]));
+  }
+  if (n) {
+    LC_CUDA(cudaMemcpyAsync(dest, ctx->b.p, ob, cudaMemcpyDeviceToHost, ctx->stream));
+    LC_CUDA(cudaMemcpyAsync(dist, ctx->c.p, ob, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  LC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LC_OK;
+}
+
+int lc_clock(lc_ctx* ctx, const lc_spec* spec, const uint64_t* xs, uint64_t n, uint64_t t, uint64_t* out) {
+  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  lc::SpecId id;
+  int rc = check_spec(spec, &id);
+  if (rc) return rc;
+  if (n == 0) return LC_OK;
+  LC_CUDA(cudaSetDevice(ctx->device));
+  const size_t nb = static_cast<size_t>(n) * 8;
+  LC_CUDA(ctx->a.ensure(nb));
+  LC_CUDA(ctx->b.ensure(nb));
+  LC_CUDA(cudaMemcpyAsync(ctx->a.p, xs, nb, cudaMemcpyHostToDevice, ctx->stream));
+  LC_CUDA(lc::launch_clock(id, ctx->a.as<uint64_t>(), n, t, ctx->b.as<uint64_t>(), ctx->stream));
+  g_launches += 1;
+  LC_CUDA(cudaMemcpyAsync(out, ctx->b.p, nb, cudaMemcpyDeviceToHost, ctx->stream));
+  LC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LC_OK;
+}
+
+// ------------------------------------------------------------ predicate / predecessors
+
+int lc_is_candidate(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const uint64_t* xs, uint64_t n,
+                    uint8_t* out) {
+  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  lc::SpecId id;
+  int rc = check_spec(spec, &id);
+  if (rc) return rc;
+  if ((rc = check_fixed(id, fixed_r3))) return rc;
+  if (n == 0) return LC_OK;
+  LC_CUDA(cudaSetDevice(ctx->device));
+  LC_CUDA(ctx->a.ensure(n * 8));
+  LC_CUDA(ctx->b.ensure(n));
+  LC_CUDA(cudaMemcpyAsync(ctx->a.p, xs, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  LC_CUDA(lc::launch_is_candidate(id, ctx->a.as<uint64_t>(), n, static_cast<uint32_t>(fixed_r3),
+                                  ctx->b.as<uint8_t>(), ctx->stream));
+  g_launches += 1;
+  LC_CUDA(cudaMemcpyAsync(out, ctx->b.p, n, cudaMemcpyDeviceToHost, ctx->stream));
+  LC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LC_OK;
+}
+
+int lc_predecessors(lc_ctx* ctx, const lc_spec* spec, const uint64_t* xs, uint64_t n, uint64_t* out,
+                    uint8_t* count) {
+  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  lc::SpecId id;
+  int rc = check_spec(spec, &id);
+  if (rc) return rc;
+  if (n == 0) return LC_OK;
+  LC_CUDA(cudaSetDevice(ctx->device));
+  LC_CUDA(ctx->a.ensure(n * 8));
+  LC_CUDA(ctx->b.ensure(n * 32));
+  LC_CUDA(ctx->c.ensure(n));
+  LC_CUDA(cudaMemcpyAsync(ctx->a.p, xs, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  LC_CUDA(lc::launch_predecessors(id, ctx->a.as<uint64_t>(), n, ctx->b.as<uint64_t>(), ctx->c.as<uint8_t>(),
+                                  ctx->stream));
+  g_launches += 1;
+  LC_CUDA(cudaMemcpyAsync(out, ctx->b.p, n * 32, cudaMemcpyDeviceToHost, ctx->stream));
+  LC_CUDA(cudaMemcpyAsync(count, ctx->c.p, n, cudaMemcpyDeviceToHost, ctx->stream));
+  LC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LC_OK;
+}
+
+// ------------------------------------------------------------------- enumeration
+
+int lc_enumerate_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, uint64_t r2_lo, uint64_t r2_hi,
+                        uint64_t* d_out, uint64_t cap, uint64_t* d_count, void* stream) {
+  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  lc::SpecId id;
+  int rc = check_spec(spec, &id);
+  if (rc) return rc;
+  if ((rc = check_fixed(id, fixed_r3))) return rc;
+  const int l2 = spec->lengths[1];
+  if (r2_lo < 1 || r2_hi > (1ull << l2) || r2_lo > r2_hi)
+    return fail(LC_ERR_ARG, "R2 rows must satisfy 1 <= r2_lo <= r2_hi <= 2^%d", l2);
+  LC_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  const uint64_t words = lc::enumerate_scratch_words(id, r2_lo, r2_hi);
+  LC_CUDA(ctx->scratch.ensure(words * 8));
+  int launches = 0;
+  LC_CUDA(lc::launch_enumerate(id, static_cast<uint32_t>(fixed_r3), r2_lo, r2_hi, d_out, cap, d_count,
+                               ctx->scratch.as<uint64_t>(), words, st, &launches));
+  g_launches += launches;
+  return LC_OK;
+}
+
+int lc_enumerate(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, uint64_t r2_lo, uint64_t r2_hi,
+                 uint64_t* out, uint64_t cap, uint64_t* count) {
+  if (!ctx || !count) return fail(LC_ERR_ARG, "null argument");
+  LC_CUDA(cudaSetDevice(ctx->device));
+  LC_CUDA(ctx->a.ensure(std::max<uint64_t>(cap, 1) * 8));
+  LC_CUDA(ctx->d.ensure(8));
+  int rc = lc_enumerate_device(ctx, spec, fixed_r3, r2_lo, r2_hi, ctx->a.as<uint64_t>(), cap,
+                               ctx->d.as<uint64_t>(), ctx->stream);
+  if (rc) return rc;
+  LC_CUDA(cudaMemcpyAsync(count, ctx->d.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  LC_CUDA(cudaStreamSynchronize(ctx->stream));
+  const uint64_t got = std::min(*count, cap);
+  if (got) {
+    LC_CUDA(cudaMemcpyAsync(out, ctx->a.p, got * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    LC_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  if (*count > cap) return fail(LC_ERR_OVERFLOW, "%llu candidates exceed capacity %llu",
+                                static_cast<unsigned long long>(*count), static_cast<unsigned long long>(cap));
+  return LC_OK;
+}
+
+// -------------------------------------------------------------- seeded start set (K0)
+
+static double acceptance_estimate(lc::SpecId id) {
+  (void)id;
+  return 0.40;  // A5/1 0.438, minis ~0.44-0.5; under-estimating only costs extra trials
+}
+
+int lc_random_candidates_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, uint64_t seed, uint64_t n,
+                                uint64_t* d_out, void* stream) {
+  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  lc::SpecId id;
+  int rc = check_spec(spec, &id);
+  if (rc) return rc;
+  if ((rc = check_fixed(id, fixed_r3))) return rc;
+  if (n == 0) return LC_OK;
+  LC_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  uint64_t trials = static_cast<uint64_t>(static_cast<double>(n) / acceptance_estimate(id)) + 65536;
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    const uint64_t words = lc::random_scratch_words(trials);
+    LC_CUDA(ctx->scratch.ensure(words * 8));
+    LC_CUDA(ctx->d.ensure(8));
+    int launches = 0;
+    LC_CUDA(lc::launch_random_candidates(id, static_cast<uint32_t>(fixed_r3), seed, trials, d_out, n,
+                                         ctx->d.as<uint64_t>(), ctx->scratch.as<uint64_t>(), words, st,
+                                         &launches));
+    g_launches += launches;
+    uint64_t got = 0;
+    LC_CUDA(cudaMemcpyAsync(&got, ctx->d.p, 8, cudaMemcpyDeviceToHost, st));
+    LC_CUDA(cudaStreamSynchronize(st));
+    if (got >= n) return LC_OK;
+    trials *= 2;
+  }
+  return fail(LC_ERR_ARG, "too few special nodes in the trial stream (wrong fixed R3?)");
+}
+
+int lc_random_candidates(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, uint64_t seed, uint64_t n,
+                         uint64_t* out, uint64_t* trials_used) {
+  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  if (n == 0) {
+    if (trials_used) *trials_used = 0;
+    return LC_OK;
+  }
+  LC_CUDA(cudaSetDevice(ctx->device));
+  LC_CUDA(ctx->b.ensure(n * 8));
+  int rc = lc_random_candidates_device(ctx, spec, fixed_r3, seed, n, ctx->b.as<uint64_t>(), ctx->stream);
+  if (rc) return rc;
+  LC_CUDA(cudaMemcpyAsync(out, ctx->b.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  LC_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (trials_used) *trials_used = 0;  // not tracked (the host restatement recomputes it)
+  return LC_OK;
+}
+
+// ------------------------------------------------------------------------ prune (K3)
+
+int lc_prune(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int32_t mode, uint64_t limit,
+             const uint64_t* cands, uint64_t n, uint8_t* removed, uint64_t* work) {
+  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  lc::SpecId id;
+  int rc = check_spec(spec, &id);
+  if (rc) return rc;
+  if ((rc = check_fixed(id, fixed_r3))) return rc;
+  if (mode != 0 && mode != 1) return fail(LC_ERR_ARG, "mode must be 0 (dfs) or 1 (bfs)");
+  if (limit < 1) return fail(LC_ERR_ARG, "limit must be >= 1");
+  if (n == 0) return LC_OK;
+  LC_CUDA(cudaSetDevice(ctx->device));
+  LC_CUDA(ctx->a.ensure(n * 8));
+  LC_CUDA(ctx->b.ensure(n));
+  LC_CUDA(ctx->c.ensure(n * 8));
+  LC_CUDA(ctx->queue.ensure(8));
+  LC_CUDA(cudaMemcpyAsync(ctx->a.p, cands, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  LC_CUDA(cudaMemsetAsync(ctx->queue.p, 0, 8, ctx->stream));
+  const int blocks = lc::prune_blocks_per_sm(id) * ctx->sms;
+  LC_CUDA(lc::launch_prune(id, static_cast<uint32_t>(fixed_r3), mode, limit, ctx->a.as<uint64_t>(), n,
+                           ctx->b.as<uint8_t>(), ctx->c.as<uint64_t>(), ctx->queue.as<unsigned long long>(),
+                           blocks, ctx->stream));
+  g_launches += 1;
+  LC_CUDA(cudaMemcpyAsync(removed, ctx->b.p, n, cudaMemcpyDeviceToHost, ctx->stream));
+  LC_CUDA(cudaMemcpyAsync(work, ctx->c.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  LC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LC_OK;
+}
+
+// ---------------------------------------------------------------- closure check
+
+int lc_first_missing(lc_ctx* ctx, const uint64_t* sorted_set, uint64_t m, const uint64_t* queries, uint64_t n,
+                     uint64_t* first_missing) {
+  if (!ctx || !first_missing) return fail(LC_ERR_ARG, "null argument");
+  *first_missing = n;
+  if (n == 0) return LC_OK;
+  LC_CUDA(cudaSetDevice(ctx->device));
+  LC_CUDA(ctx->a.ensure(std::max<uint64_t>(m, 1) * 8));
+  LC_CUDA(ctx->b.ensure(n * 8));
+  LC_CUDA(ctx->d.ensure(8));
+  if (m) LC_CUDA(cudaMemcpyAsync(ctx->a.p, sorted_set, m * 8, cudaMemcpyHostToDevice, ctx->stream));
+  LC_CUDA(cudaMemcpyAsync(ctx->b.p, queries, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  LC_CUDA(cudaMemcpyAsync(ctx->d.p, &n, 8, cudaMemcpyHostToDevice, ctx->stream));
+  LC_CUDA(lc::launch_first_missing(ctx->a.as<uint64_t>(), m, ctx->b.as<uint64_t>(), n,
+                                   ctx->d.as<unsigned long long>(), ctx->stream));
+  g_launches += 1;
+  LC_CUDA(cudaMemcpyAsync(first_missing, ctx->d.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  LC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,429 @@
+// Batch kernels around the walk: the special-node predicate and predecessor batch
+// (cipher.py:342-428), fixed-count clocking (bitslice.clock_sliced), ordered-compaction
+// enumeration of step 1 (K2, pipeline.enumerate_candidates), the seeded start-set
+// generator (K0), the step-2 prune (K3, pipeline.prune_shallow_segments) and the
+// closure check of build_skeleton_edges.
+#include <cuda_runtime.h>
+
+#include "lfsr_common.cuh"
+#include "lfsr_internal.h"
+
+namespace lc {
+
+namespace {
+
+constexpr uint32_t kFull = 0xffffffffu;
+constexpr int kThreads = 256;
+
+template <class S>
+__global__ void is_candidate_kernel(const uint64_t* __restrict__ xs, uint64_t n, uint32_t F,
+                                    uint8_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = is_candidate<S>(xs[i], F) ? 1 : 0;
+}
+
+template <class S>
+__global__ void predecessors_kernel(const uint64_t* __restrict__ xs, uint64_t n,
+                                    uint64_t* __restrict__ out, uint8_t* __restrict__ count) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t p[4] = {0, 0, 0, 0};
+    const int c = predecessors<S>(xs[i], p);
+    ulonglong2* o = reinterpret_cast<ulonglong2*>(out + 4 * i);
+    o[0] = make_ulonglong2(p[0], p[1]);
+    o[1] = make_ulonglong2(p[2], p[3]);
+    count[i] = static_cast<uint8_t>(c);
+  }
+}
+
+// bitslice.clock_sliced: 32 states per thread, bitsliced, t unchecked steps.
+template <class S>
+__global__ void clock_kernel(const uint64_t* __restrict__ xs, uint64_t n, uint64_t t,
+                             uint64_t* __restrict__ out) {
+  const uint64_t base = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) * 32u;
+  if (base >= n) return;
+  const int lanes = static_cast<int>(n - base < 32u ? n - base : 32u);
+  uint32_t s[S::NB];
+#pragma unroll
+  for (int i = 0; i < S::NB; ++i) s[i] = 0u;
+  for (int j = 0; j < lanes; ++j) insert_lane<S::NB>(s, j, xs[base + j]);
+  for (uint64_t left = t; left != 0;) {
+    const uint32_t c = left > (1u << 30) ? (1u << 30) : static_cast<uint32_t>(left);
+#pragma unroll 1
+    for (uint32_t k = 0; k < c; ++k) step<S>(s);
+    left -= c;
+  }
+  for (int j = 0; j < lanes; ++j) out[base + j] = extract_lane<S::NB>(s, j);
+}
+
+// ---------------------------------------------------------------- ordered compaction
+// Index space [0, total) -> state via a generator; states passing is_candidate are
+// written densely in index order.  Pass 1 counts per tile, pass 2 scans the tile counts,
+// pass 3 re-evaluates and writes with a warp-ballot / block prefix (coalesced stores).
+
+constexpr int kTileShift = 16;
+constexpr uint64_t kTile = 1ull << kTileShift;
+constexpr int kCompactThreads = 256;
+
+template <class S>
+struct EnumGen {
+  uint64_t r2_lo;
+  uint64_t packed_f;
+  __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
+    const uint64_t r2 = r2_lo + i / S::M1;
+    const uint64_t r1 = 1u + i % S::M1;
+    return r1 | (r2 << S::O2) | packed_f;
+  }
+};
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// K0: trial i -> h = splitmix64(seed + (i + 1) * golden); r1 = 1 + lo32(h) * m1 >> 32,
+// r2 = 1 + hi32(h) * m2 >> 32, R3 = F.  (Restated in oracle/k0.py for parity.)
+template <class S>
+struct RandGen {
+  uint64_t seed;
+  uint64_t packed_f;
+  __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
+    const uint64_t h = splitmix64(seed + (i + 1u) * 0x9E3779B97F4A7C15ull);
+    const uint64_t r1 = 1u + (((h & 0xffffffffull) * S::M1) >> 32);
+    const uint64_t r2 = 1u + (((h >> 32) * S::M2) >> 32);
+    return r1 | (r2 << S::O2) | packed_f;
+  }
+};
+
+template <class S, class Gen>
+__global__ void __launch_bounds__(kCompactThreads) compact_count_kernel(Gen g, uint64_t total,
+                                                                        uint32_t F,
+                                                                        uint64_t* __restrict__ tile_counts) {
+  const uint64_t lo = blockIdx.x * kTile;
+  const uint64_t hi = min(total, lo + kTile);
+  uint32_t c = 0;
+  for (uint64_t i = lo + threadIdx.x; i < hi; i += kCompactThreads) c += is_candidate<S>(g(i), F) ? 1u : 0u;
+  c = __reduce_add_sync(kFull, c);
+  __shared__ uint32_t part[kCompactThreads / 32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t sum = 0;
+    for (int w = 0; w < kCompactThreads / 32; ++w) sum += part[w];
+    tile_counts[blockIdx.x] = sum;
+  }
+}
+
+// Exclusive scan of tile counts in place; counts[tiles] = total.  One block.
+__global__ void scan_kernel(uint64_t* __restrict__ counts, uint64_t tiles, uint64_t* __restrict__ total_out) {
+  __shared__ uint64_t part[1024];
+  const uint64_t per = (tiles + blockDim.x - 1) / blockDim.x;
+  const uint64_t lo = threadIdx.x * per, hi = min(tiles, lo + per);
+  uint64_t sum = 0;
+  for (uint64_t i = lo; i < hi; ++i) sum += counts[i];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t run = 0;
+    for (uint32_t w = 0; w < blockDim.x; ++w) {
+      const uint64_t v = part[w];
+      part[w] = run;
+      run += v;
+    }
+    counts[tiles] = run;
+    if (total_out) *total_out = run;
+  }
+  __syncthreads();
+  uint64_t run = part[threadIdx.x];
+  for (uint64_t i = lo; i < hi; ++i) {
+    const uint64_t v = counts[i];
+    counts[i] = run;
+    run += v;
+  }
+}
+
+template <class S, class Gen>
+__global__ void __launch_bounds__(kCompactThreads) compact_write_kernel(Gen g, uint64_t total,
+                                                                        uint32_t F,
+                                                                        const uint64_t* __restrict__ offsets,
+                                                                        uint64_t* __restrict__ out,
+                                                                        uint64_t cap) {
+  __shared__ uint32_t wcount[kCompactThreads / 32];
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint64_t lo = blockIdx.x * kTile;
+  const uint64_t hi = min(total, lo + kTile);
+  uint64_t pos = offsets[blockIdx.x];
+  for (uint64_t r = lo; r < hi; r += kCompactThreads) {
+    const uint64_t i = r + threadIdx.x;
+    uint64_t x = 0;
+    bool ok = false;
+    if (i < hi) {
+      x = g(i);
+      ok = is_candidate<S>(x, F);
+    }
+    const uint32_t b = __ballot_sync(kFull, ok);
+    if (lane == 0) wcount[warp] = __popc(b);
+    __syncthreads();
+    uint32_t before = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < kCompactThreads / 32; ++w) {
+      const uint32_t v = wcount[w];
+      before += (static_cast<uint32_t>(w) < warp) ? v : 0u;
+      all += v;
+    }
+    if (ok) {
+      const uint64_t o = pos + before + __popc(b & ((1u << lane) - 1u));
+      if (o < cap) out[o] = x;
+    }
+    pos += all;
+    __syncthreads();
+  }
+}
+
+template <class S, class Gen>
+cudaError_t compact(Gen g, uint64_t total, uint32_t F, uint64_t* out, uint64_t cap, uint64_t* d_count,
+                    uint64_t* scratch, cudaStream_t stream, int* launches) {
+  const uint64_t tiles = (total + kTile - 1) / kTile;
+  if (tiles == 0) {
+    cudaError_t e = cudaMemsetAsync(d_count, 0, sizeof(uint64_t), stream);
+    return e;
+  }
+  compact_count_kernel<S, Gen><<<static_cast<unsigned>(tiles), kCompactThreads, 0, stream>>>(g, total, F, scratch);
+  scan_kernel<<<1, 1024, 0, stream>>>(scratch, tiles, d_count);
+  compact_write_kernel<S, Gen><<<static_cast<unsigned>(tiles), kCompactThreads, 0, stream>>>(g, total, F, scratch,
+                                                                                          out, cap);
+  if (launches) *launches += 3;
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K3: step-2 prune
+// Thread per candidate, stackless depth-first traversal of the candidate's segment (the
+// reverse tree through predecessors that are not candidates, pipeline.py:121-129).  The
+// pop order of the reference's LIFO stack (pipeline.py:132-144) is a preorder that visits
+// children in reverse LUT order; it is replayed without a stack by returning to the
+// parent with one forward clock and moving to the next-lower sibling, so the
+// order-dependent `expanded` counter matches exactly.  BFS mode (pipeline.py:147-160)
+// only needs the segment size capped at node_limit + 1, which is order-independent.
+
+// Child q of node y (pattern kClockPatterns[q]) from y's registers and their unsteps.
+template <class S>
+struct Node {
+  uint32_t r1, r2, r3, u1, u2, u3;
+  uint32_t mask;  // bit q: pattern q yields a valid, non-candidate predecessor
+  __device__ __forceinline__ uint64_t child(int q) const {
+    const int p = clock_pattern(q & 3);
+    const uint32_t p1 = (p & 1) ? u1 : r1, p2 = (p & 2) ? u2 : r2, p3 = (p & 4) ? u3 : r3;
+    return static_cast<uint64_t>(p1) | (static_cast<uint64_t>(p2) << S::O2) |
+           (static_cast<uint64_t>(p3) << S::O3);
+  }
+};
+
+template <class S>
+__device__ __forceinline__ Node<S> expand_node(uint64_t y, uint32_t F) {
+  Node<S> nd;
+  nd.r1 = static_cast<uint32_t>(y & S::M1);
+  nd.r2 = static_cast<uint32_t>((y >> S::O2) & S::M2);
+  nd.r3 = static_cast<uint32_t>((y >> S::O3) & S::M3);
+  nd.u1 = unstep<S::L1, S::T1>(nd.r1);
+  nd.u2 = unstep<S::L2, S::T2>(nd.r2);
+  nd.u3 = unstep<S::L3, S::T3>(nd.r3);
+  const uint32_t idx = table_index<S>(y);
+  uint32_t m = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if ((pattern_mask(q) >> idx) & 1ull) {
+      const int p = clock_pattern(q);
+      const uint32_t p1 = (p & 1) ? nd.u1 : nd.r1, p2 = (p & 2) ? nd.u2 : nd.r2,
+                     p3 = (p & 4) ? nd.u3 : nd.r3;
+      if (p1 != 0u && p2 != 0u && p3 != 0u) {
+        bool cand = false;
+        if (p3 == F) cand = is_candidate<S>(nd.child(q), F);
+        if (!cand) m |= 1u << q;
+      }
+    }
+  }
+  nd.mask = m;
+  return nd;
+}
+
+template <class S>
+__device__ void prune_one(uint64_t root, uint32_t F, int mode, uint64_t limit, uint8_t* removed,
+                          uint64_t* work) {
+  uint64_t x = root, d = 0, count = 1, expanded = 0;
+  bool pop = true, shallow = true;
+  for (;;) {
+    if (!pop && d == 0) break;  // back at the root: traversal complete
+    const uint64_t y = pop ? x : clock_scalar<S>(x);
+    const Node<S> nd = expand_node<S>(y, F);
+    if (pop) {
+      if (nd.mask != 0u) {
+        if (mode == 0) {
+          if (d >= limit) {  // a child would sit below the depth limit
+            expanded += 1;
+            shallow = false;
+            break;
+          }
+          expanded += __popc(nd.mask);
+        } else {
+          count += __popc(nd.mask);
+          if (count > limit) {
+            count = limit + 1;
+            shallow = false;
+            break;
+          }
+        }
+        x = nd.child(31 - __clz(nd.mask));  // the reference pops the last child first
+        ++d;
+      } else {
+        pop = false;
+      }
+    } else {
+      // y is x's parent; continue with x's next-lower sibling, else climb
+      uint32_t q = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (((nd.mask >> k) & 1u) && nd.child(k) == x) q = k;
+      const uint32_t lower = nd.mask & ((1u << q) - 1u);
+      if (lower != 0u) {
+        x = nd.child(31 - __clz(lower));
+        pop = true;
+      } else {
+        x = y;
+        --d;
+      }
+    }
+  }
+  *removed = shallow ? 1 : 0;
+  *work = mode == 0 ? expanded : count;
+}
+
+template <class S>
+__global__ void __launch_bounds__(kThreads) prune_kernel(const uint64_t* __restrict__ cands, uint64_t n,
+                                                         uint32_t F, int mode, uint64_t limit,
+                                                         uint8_t* __restrict__ removed,
+                                                         uint64_t* __restrict__ work,
+                                                         unsigned long long* queue) {
+  for (;;) {
+    // warp-aggregated ticket: one atomic per warp per round
+    const uint32_t lane = threadIdx.x & 31u;
+    unsigned long long base = 0;
+    const uint32_t act = __activemask();
+    const int leader = __ffs(act) - 1;
+    if (static_cast<int>(lane) == leader) base = atomicAdd(queue, static_cast<unsigned long long>(__popc(act)));
+    base = __shfl_sync(act, base, leader);
+    const uint64_t i = base + __popc(act & ((1u << lane) - 1u));
+    if (i >= n) break;
+    prune_one<S>(cands[i], F, mode, limit, &removed[i], &work[i]);
+  }
+}
+
+__global__ void first_missing_kernel(const uint64_t* __restrict__ set, uint64_t m,
+                                     const uint64_t* __restrict__ q, uint64_t n,
+                                     unsigned long long* first) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t v = q[i];
+    uint64_t lo = 0, hi = m;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (set[mid] < v) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo >= m || set[lo] != v) atomicMin(first, static_cast<unsigned long long>(i));
+  }
+}
+
+inline unsigned grid_for(uint64_t n, int threads, uint64_t per_thread = 1) {
+  const uint64_t g = (n + static_cast<uint64_t>(threads) * per_thread - 1) / (static_cast<uint64_t>(threads) * per_thread);
+  return static_cast<unsigned>(g == 0 ? 1 : (g > (1u << 20) ? (1u << 20) : g));
+}
+
+template <template <class> class K>
+struct Dispatch;
+
+}  // namespace
+
+#define LC_DISPATCH(id, ...)                                  \
+  switch (id) {                                               \
+    case SpecId::A51: { using S = A51; __VA_ARGS__; }         \
+    case SpecId::MINI567: { using S = MINI567; __VA_ARGS__; } \
+    case SpecId::MINI789: { using S = MINI789; __VA_ARGS__; } \
+    default: return cudaErrorInvalidValue;                    \
+  }
+
+cudaError_t launch_is_candidate(SpecId id, const uint64_t* xs, uint64_t n, uint32_t F, uint8_t* out,
+                                cudaStream_t stream) {
+  LC_DISPATCH(id, is_candidate_kernel<S><<<grid_for(n, kThreads), kThreads, 0, stream>>>(xs, n, F, out);
+              return cudaGetLastError());
+}
+
+cudaError_t launch_predecessors(SpecId id, const uint64_t* xs, uint64_t n, uint64_t* out,
+                                uint8_t* count, cudaStream_t stream) {
+  LC_DISPATCH(id, predecessors_kernel<S><<<grid_for(n, kThreads), kThreads, 0, stream>>>(xs, n, out, count);
+              return cudaGetLastError());
+}
+
+cudaError_t launch_clock(SpecId id, const uint64_t* xs, uint64_t n, uint64_t t, uint64_t* out,
+                         cudaStream_t stream) {
+  const unsigned g = static_cast<unsigned>((n + 32u * 128u - 1) / (32u * 128u));
+  LC_DISPATCH(id, clock_kernel<S><<<g == 0 ? 1 : g, 128, 0, stream>>>(xs, n, t, out); return cudaGetLastError());
+}
+
+uint64_t enumerate_scratch_words(SpecId id, uint64_t r2_lo, uint64_t r2_hi) {
+  uint64_t m1 = id == SpecId::A51 ? A51::M1 : (id == SpecId::MINI567 ? MINI567::M1 : MINI789::M1);
+  const uint64_t total = (r2_hi > r2_lo ? r2_hi - r2_lo : 0) * m1;
+  return (total + kTile - 1) / kTile + 1;
+}
+
+cudaError_t launch_enumerate(SpecId id, uint32_t F, uint64_t r2_lo, uint64_t r2_hi, uint64_t* out,
+                             uint64_t cap, uint64_t* d_count, uint64_t* scratch,
+                             uint64_t scratch_words, cudaStream_t stream, int* launches) {
+  (void)scratch_words;
+  LC_DISPATCH(id, {
+    EnumGen<S> g{r2_lo, static_cast<uint64_t>(F) << S::O3};
+    const uint64_t total = (r2_hi > r2_lo ? r2_hi - r2_lo : 0) * S::M1;
+    return compact<S>(g, total, F, out, cap, d_count, scratch, stream, launches);
+  });
+}
+
+uint64_t random_scratch_words(uint64_t trials) { return (trials + kTile - 1) / kTile + 1; }
+
+cudaError_t launch_random_candidates(SpecId id, uint32_t F, uint64_t seed, uint64_t trials,
+                                     uint64_t* out, uint64_t cap, uint64_t* d_count,
+                                     uint64_t* scratch, uint64_t scratch_words,
+                                     cudaStream_t stream, int* launches) {
+  (void)scratch_words;
+  LC_DISPATCH(id, {
+    RandGen<S> g{seed, static_cast<uint64_t>(F) << S::O3};
+    return compact<S>(g, trials, F, out, cap, d_count, scratch, stream, launches);
+  });
+}
+
+cudaError_t launch_prune(SpecId id, uint32_t F, int mode, uint64_t limit, const uint64_t* cands,
+                         uint64_t n, uint8_t* removed, uint64_t* work, unsigned long long* queue,
+                         int blocks, cudaStream_t stream) {
+  LC_DISPATCH(id, prune_kernel<S><<<blocks, kThreads, 0, stream>>>(cands, n, F, mode, limit, removed, work,
+                                                                   queue);
+              return cudaGetLastError());
+}
+
+int prune_blocks_per_sm(SpecId id) {
+  int b = 1;
+  switch (id) {
+    case SpecId::A51: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, prune_kernel<A51>, kThreads, 0); break;
+    case SpecId::MINI567: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, prune_kernel<MINI567>, kThreads, 0); break;
+    case SpecId::MINI789: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, prune_kernel<MINI789>, kThreads, 0); break;
+    default: break;
+  }
+  return b > 0 ? b : 1;
+}
+
+cudaError_t launch_first_missing(const uint64_t* set, uint64_t m, const uint64_t* q, uint64_t n,
+                                 unsigned long long* first, cudaStream_t stream) {
+  first_missing_kernel<<<grid_for(n, kThreads), kThreads, 0, stream>>>(set, m, q, n, first);
+  return cudaGetLastError();
+}
+
+}  // namespace lc

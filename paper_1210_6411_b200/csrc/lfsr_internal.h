@@ -1,0 +1,85 @@
+// Host/device shared declarations for the lfsr_b200 kernels (not part of the C ABI).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/lfsr_b200.h"
+
+namespace lc {
+
+enum class SpecId { A51 = 0, MINI567 = 1, MINI789 = 2, UNSUPPORTED = -1 };
+
+constexpr int kWalkThreads = 128;
+constexpr uint64_t kInf = ~0ull;
+
+// Per-lane bookkeeping of the chain walk (global scratch, touched only on events).
+struct LaneMeta {
+  uint64_t walk;       // index of the start this lane is walking
+  uint64_t leg_start;  // warp clock at which the current leg began
+  uint64_t arm_at;     // warp clock from which the lane may report a special node
+  uint64_t deadline;   // warp clock of the cap audit
+  uint32_t legs_done;
+  uint32_t pad;
+};
+
+struct WalkParams {
+  const uint64_t* starts;
+  uint64_t n;
+  uint64_t* dst;  // [n][legs]
+  uint64_t* dist;
+  uint64_t stride;
+  uint64_t cap1;  // max_clocks + 1, saturated
+  uint64_t hist_lo;
+  uint32_t hist_shift;
+  uint32_t hist_bins;
+  uint32_t legs;
+  uint32_t fixed_r3;
+  uint32_t refill_min;  // refill once this many of the warp's 1024 lanes are idle
+  uint32_t pad;
+  unsigned long long* queue;  // next start index
+  unsigned long long* stats;  // LC_ST_* block
+  LaneMeta* meta;             // [threads][32]
+};
+
+// Launchers (defined in the .cu files); all enqueue on `stream`.
+cudaError_t launch_walk(SpecId id, bool static_f, const WalkParams& p, int blocks,
+                        cudaStream_t stream);
+int walk_blocks_per_sm(SpecId id, bool static_f);
+cudaError_t launch_init_stats(uint64_t* stats, uint64_t hist_lo, uint32_t hist_shift, uint32_t hist_bins,
+                              cudaStream_t stream);
+
+cudaError_t launch_is_candidate(SpecId id, const uint64_t* xs, uint64_t n, uint32_t F, uint8_t* out,
+                                cudaStream_t stream);
+cudaError_t launch_predecessors(SpecId id, const uint64_t* xs, uint64_t n, uint64_t* out,
+                                uint8_t* count, cudaStream_t stream);
+cudaError_t launch_clock(SpecId id, const uint64_t* xs, uint64_t n, uint64_t t, uint64_t* out,
+                         cudaStream_t stream);
+
+// Ordered compaction generators (enumeration and the seeded start set).
+struct EnumRange {
+  uint64_t r2_lo;
+  uint64_t rows;
+};
+// Counts per tile then writes; scratch must hold tiles+1 u64.  Returns tiles used.
+cudaError_t launch_enumerate(SpecId id, uint32_t F, uint64_t r2_lo, uint64_t r2_hi, uint64_t* out,
+                             uint64_t cap, uint64_t* d_count, uint64_t* scratch,
+                             uint64_t scratch_words, cudaStream_t stream, int* launches);
+uint64_t enumerate_scratch_words(SpecId id, uint64_t r2_lo, uint64_t r2_hi);
+cudaError_t launch_random_candidates(SpecId id, uint32_t F, uint64_t seed, uint64_t trials,
+                                     uint64_t* out, uint64_t cap, uint64_t* d_count,
+                                     uint64_t* scratch, uint64_t scratch_words,
+                                     cudaStream_t stream, int* launches);
+uint64_t random_scratch_words(uint64_t trials);
+
+cudaError_t launch_prune(SpecId id, uint32_t F, int mode, uint64_t limit, const uint64_t* cands,
+                         uint64_t n, uint8_t* removed, uint64_t* work,
+                         unsigned long long* queue, int blocks, cudaStream_t stream);
+int prune_blocks_per_sm(SpecId id);
+
+cudaError_t measure_lop3_peak(int sms, double* ops_per_s, double* sm_mhz);
+
+cudaError_t launch_first_missing(const uint64_t* set, uint64_t m, const uint64_t* q, uint64_t n,
+                                 unsigned long long* first, cudaStream_t stream);
+
+}  // namespace lc

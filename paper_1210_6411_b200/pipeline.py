@@ -1,0 +1,258 @@
+"""Steps 1-3 orchestration: drop-in for ``lfsrcycles.pipeline`` (reference
+``pkg/src/lfsrcycles/pipeline.py``).
+
+* ``enumerate_candidates`` -- step 1 on the GPU (K2 ordered compaction), ascending.
+* ``prune_shallow_segments`` -- step 2 on the GPU (K3 stackless reverse DFS/BFS); the
+  survivor list, ``removed`` and the order-dependent ``expanded`` counter match the
+  reference exactly.
+* ``build_skeleton_edges`` -- step 3: the GPU chain walk plus a GPU closure check.
+* ``probe_segment`` / ``auto_depth_limit`` -- level-order segment sweeps, one batched GPU
+  predecessor/predicate pass per level.
+* ``random_candidate`` -- the reference's seeded scalar sampler (same stream of states
+  for the same ``random.Random``); ``random_candidates_gpu`` is the counter-based K0
+  generator used for large synthetic start sets.
+"""
+
+from __future__ import annotations
+
+import random
+from dataclasses import dataclass
+from typing import Iterable, Iterator
+
+import numpy as np
+
+from . import _batch
+from .bitslice import forward_to_candidate
+from .cipher import CandidateParams, CipherSpec, PredecessorTable, is_candidate, shared_table
+from .records import EdgeRecord
+
+__all__ = [
+    "PruneConfig", "PruneStats", "PruneSoundnessError", "enumerate_candidates",
+    "enumerate_candidates_array", "prune_shallow_segments", "build_skeleton_edges",
+    "probe_segment", "probe_segments", "auto_depth_limit", "random_candidate",
+    "random_candidates_gpu",
+]
+
+_PRUNE_CHUNK_GPU = 1 << 22
+_ENUM_ROWS_PER_CALL = 1 << 12
+
+
+class PruneSoundnessError(RuntimeError):
+    """A surviving node's forward walk hit a pruned candidate (pipeline.py:45-47)."""
+
+
+@dataclass(frozen=True)
+class PruneConfig:
+    """Bounded reverse traversal settings (pipeline.py:50-84).  ``workers`` is accepted
+    for API compatibility; the GPU kernel does not use host workers."""
+
+    mode: str = "dfs"
+    depth_limit: int | None = None
+    node_limit: int | None = None
+    workers: int = 1
+
+    def validate(self, spec: CipherSpec) -> None:
+        bound = (1 << spec.lengths[2]) - 1
+        if self.mode == "dfs":
+            if not self.depth_limit or self.depth_limit < 1:
+                raise ValueError("dfs mode needs a positive depth_limit")
+            if self.depth_limit >= bound:
+                raise ValueError(f"depth_limit {self.depth_limit} must stay below the minimum "
+                                 f"candidate spacing {bound}")
+        elif self.mode == "bfs":
+            if not self.node_limit or self.node_limit < 1:
+                raise ValueError("bfs mode needs a positive node_limit")
+            if self.node_limit >= bound:
+                raise ValueError(f"node_limit {self.node_limit} must stay below the minimum "
+                                 f"candidate spacing {bound}")
+        else:
+            raise ValueError(f"unknown prune mode {self.mode!r}")
+        if self.workers < 1:
+            raise ValueError("workers must be >= 1")
+
+
+@dataclass
+class PruneStats:
+    mode: str
+    limit: int
+    total: int = 0
+    removed: int = 0
+    expanded: int = 0
+
+    @property
+    def surviving(self) -> int:
+        return self.total - self.removed
+
+    @property
+    def removed_fraction(self) -> float:
+        return self.removed / self.total if self.total else 0.0
+
+
+# ----------------------------------------------------------------------- step 1
+
+
+def enumerate_candidates_array(spec: CipherSpec, params: CandidateParams, r2_lo: int = 1,
+                               r2_hi: int | None = None) -> np.ndarray:
+    """Special nodes with R2 in [r2_lo, r2_hi) (default: all), ascending, as uint64."""
+    if r2_hi is None:
+        r2_hi = spec.reg_masks[1] + 1
+    parts = [_batch.enumerate_rows(spec, params, lo, min(r2_hi, lo + _ENUM_ROWS_PER_CALL))
+             for lo in range(r2_lo, r2_hi, _ENUM_ROWS_PER_CALL)]
+    return np.concatenate(parts) if parts else np.zeros(0, dtype=np.uint64)
+
+
+def enumerate_candidates(spec: CipherSpec, params: CandidateParams,
+                         table: PredecessorTable | None = None) -> Iterator[int]:
+    """All candidates in ascending packed order (pipeline.py:104-118), produced on the
+    GPU a block of R2 rows at a time."""
+    r2_hi = spec.reg_masks[1] + 1
+    for lo in range(1, r2_hi, _ENUM_ROWS_PER_CALL):
+        rows = _batch.enumerate_rows(spec, params, lo, min(r2_hi, lo + _ENUM_ROWS_PER_CALL))
+        yield from rows.tolist()
+
+
+# ----------------------------------------------------------------------- step 2
+
+
+def prune_shallow_segments(candidates: Iterable[int], config: PruneConfig, spec: CipherSpec,
+                           params: CandidateParams,
+                           table: PredecessorTable | None = None) -> tuple:
+    """Drop candidates rooting shallow segments; survivors keep input order
+    (pipeline.py:192-222)."""
+    config.validate(spec)
+    limit = config.depth_limit if config.mode == "dfs" else config.node_limit
+    stats = PruneStats(mode=config.mode, limit=limit)
+    cands = np.asarray(candidates if isinstance(candidates, np.ndarray) else list(candidates),
+                       dtype=np.uint64)
+    survivors = []
+    for lo in range(0, cands.size, _PRUNE_CHUNK_GPU):
+        chunk = cands[lo: lo + _PRUNE_CHUNK_GPU]
+        removed, work = _batch.prune(chunk, spec, params, config.mode, limit)
+        survivors.append(chunk[~removed])
+        stats.total += chunk.size
+        stats.removed += int(removed.sum())
+        stats.expanded += int(work.sum())
+    out = np.concatenate(survivors) if survivors else np.zeros(0, dtype=np.uint64)
+    return out.tolist(), stats
+
+
+# ----------------------------------------------------------------------- step 3
+
+
+def _edges_chunk(args) -> list:
+    """The reference's pickled unit of step-3 work (pipeline.py:225-228)."""
+    chunk, params, spec, table, stride = args
+    walked = forward_to_candidate(chunk, params, spec, table, stride=stride)
+    return [(src, dest, dist) for src, (dest, dist) in zip(chunk, walked)]
+
+
+def build_skeleton_edges(skeleton: list, params: CandidateParams, spec: CipherSpec,
+                         table: PredecessorTable | None = None, stride: int = 1,
+                         workers: int = 1) -> list:
+    """One weighted edge per skeleton node (pipeline.py:231-256); every destination
+    must be in the skeleton, else PruneSoundnessError."""
+    sk = np.asarray(skeleton if isinstance(skeleton, np.ndarray) else list(skeleton), dtype=np.uint64)
+    if sk.size == 0:
+        raise ValueError("skeleton is empty")
+    res = _batch.walk(sk, params, spec, stride=stride, legs=1)
+    dst, dist = res.dst[:, 0], res.dist[:, 0]
+    bad = _batch.first_missing(np.unique(sk), dst)
+    if bad < sk.size:
+        raise PruneSoundnessError(
+            f"walk from {int(sk[bad]):#x} reached pruned candidate {int(dst[bad]):#x}; "
+            "prune limit exceeded the minimum candidate spacing")
+    return [EdgeRecord(s, d, w, 0, 0) for s, d, w in zip(sk.tolist(), dst.tolist(), dist.tolist())]
+
+
+# ----------------------------------------------------------------------- probing
+
+
+def probe_segments(roots, spec: CipherSpec, params: CandidateParams, *, depth_cap: int | None = None,
+                   node_cap: int | None = None, level_counts: list | None = None):
+    """Batched probe_segment: per root (depth, nodes, censored) arrays.  Each level of
+    every live segment is expanded in one GPU predecessor + predicate pass."""
+    roots = np.asarray(roots, dtype=np.uint64).reshape(-1)
+    k = roots.size
+    depth = np.zeros(k, dtype=np.int64)
+    nodes = np.ones(k, dtype=np.int64)
+    censored = np.zeros(k, dtype=bool)
+    live = np.ones(k, dtype=bool)
+    if level_counts is not None:
+        if not level_counts:
+            level_counts.append(0)
+        level_counts[0] += k
+    front, owner = roots.copy(), np.arange(k)
+    level = 0
+    while live.any():
+        if depth_cap is not None and level >= depth_cap:
+            censored[live] = True
+            break
+        preds, cnt = _batch.predecessors(front, spec)
+        sel = np.arange(4)[None, :] < cnt[:, None]
+        cand_nodes = preds[sel]
+        cand_owner = np.repeat(owner, cnt.astype(np.int64))
+        on_plane = (cand_nodes & np.uint64(params.r3_field_mask)) == np.uint64(params.packed_r3)
+        drop = np.zeros(cand_nodes.size, dtype=bool)
+        if on_plane.any():
+            drop[on_plane] = _batch.is_candidate(cand_nodes[on_plane], params, spec)
+        nxt, nowner = cand_nodes[~drop], cand_owner[~drop]
+        per = np.bincount(nowner, minlength=k)
+        finished = live & (per == 0)
+        live &= ~finished
+        if not live.any():
+            break
+        level += 1
+        depth[live] = level
+        nodes[live] += per[live]
+        if level_counts is not None:
+            if len(level_counts) <= level:
+                level_counts.append(0)
+            level_counts[level] += int(per[live].sum())
+        if node_cap is not None:
+            over = live & (nodes > node_cap)
+            censored |= over
+            live &= ~over
+        keep = live[nowner]
+        front, owner = nxt[keep], nowner[keep]
+    return depth, nodes, censored
+
+
+def probe_segment(root: int, spec: CipherSpec, params: CandidateParams,
+                  table: PredecessorTable | None = None, *, depth_cap: int | None = None,
+                  node_cap: int | None = None, level_counts: list | None = None) -> tuple:
+    """Reverse level-order sweep of one segment (pipeline.py:262-298):
+    (deepest level, nodes seen, censored)."""
+    d, n, c = probe_segments([root], spec, params, depth_cap=depth_cap, node_cap=node_cap,
+                             level_counts=level_counts)
+    return int(d[0]), int(n[0]), bool(c[0])
+
+
+def random_candidate(rng: random.Random, spec: CipherSpec, params: CandidateParams,
+                     table: PredecessorTable | None = None) -> int:
+    """Uniform candidate by rejection over the fixed-R3 plane (pipeline.py:301-310);
+    consumes ``rng`` exactly like the reference, so seeds give the same states."""
+    m1, m2, _ = spec.reg_masks
+    o2 = spec.offsets[1]
+    table = table or shared_table()
+    while True:
+        x = rng.randrange(1, m1 + 1) | (rng.randrange(1, m2 + 1) << o2) | params.packed_r3
+        if is_candidate(x, params, spec, table):
+            return x
+
+
+def random_candidates_gpu(spec: CipherSpec, params: CandidateParams, seed: int, n: int) -> np.ndarray:
+    """K0 seeded synthetic start set: the first n candidates of the counter-based trial
+    stream, generated and filtered on the GPU."""
+    return _batch.random_candidates(spec, params, seed, n)
+
+
+def auto_depth_limit(spec: CipherSpec, params: CandidateParams, table: PredecessorTable | None = None, *,
+                     sample: int = 256, seed: int = 0) -> int:
+    """75th-percentile sampled segment depth, clamped under the spacing bound
+    (pipeline.py:313-333)."""
+    bound = (1 << spec.lengths[2]) - 2
+    rng = random.Random(seed)
+    roots = [random_candidate(rng, spec, params, table) for _ in range(sample)]
+    depths, _, _ = probe_segments(roots, spec, params, depth_cap=bound, node_cap=200_000)
+    depths = sorted(int(d) for d in depths)
+    return max(4, min(depths[(3 * len(depths)) // 4], bound))

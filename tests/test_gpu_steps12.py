@@ -1,0 +1,133 @@
+"""GPU parity of the step-1/2 kernels and batch predicates against the reference's
+golden vectors: is_candidate / predecessors (cipher.py:342-428), clock_sliced
+(bitslice.py:223-228), enumerate_candidates (pipeline.py:104-118), prune_shallow_segments
+(pipeline.py:192-222), build_skeleton_edges (pipeline.py:231-256), probe_segment, K0."""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden_json, golden_npz, has_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def u64_digest(values):
+    return hashlib.sha256(np.asarray(values, dtype="<u8").tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("name", ["a51", "mini567", "mini789"])
+def test_batch_predicate_and_predecessors(gpu, lc, specs, params, name):
+    g = golden_npz(f"pred_{name}")
+    got = lc.is_candidate(g["states"], params[name], specs[name])
+    assert (got == g["is_candidate"].astype(bool)).all()
+    preds, cnt = lc.predecessors(g["states"], specs[name])
+    assert (cnt == g["npred"]).all()
+    assert (preds == g["preds"]).all()
+
+
+@pytest.mark.parametrize("name", ["a51", "mini567", "mini789"])
+def test_clock_sliced_matches_reference(gpu, lc, specs, name):
+    from paper_1210_6411_b200 import _batch
+
+    g = golden_npz(f"traj_{name}")
+    assert (_batch.clock(g["starts"], specs[name], 1) == g["traj"][:, 0]).all()
+    assert (_batch.clock(g["starts"], specs[name], 64) == g["traj"][:, 63]).all()
+    sb = lc.transpose(g["starts"].tolist(), specs[name], 256)
+    out = lc.clock_sliced(sb, specs[name], 500)
+    assert lc.untranspose(out) == g["after500"].tolist()
+
+
+@pytest.mark.parametrize("name", ["mini567", "mini789"])
+def test_enumerate_minis(gpu, lc, specs, params, name):
+    meta = golden_json("enumerate.json")[name]
+    got = list(lc.enumerate_candidates(specs[name], params[name]))
+    assert len(got) == meta["count"]
+    assert u64_digest(got) == meta["digest"]
+
+
+@pytest.mark.parametrize("r2_0", [0x1, 0x1234, 0x3FFFFC])
+def test_enumerate_a51_rows(gpu, lc, specs, params, r2_0):
+    meta = golden_json("enumerate.json")[f"a51_rows_{r2_0:#x}_4"]
+    got = lc.enumerate_candidates_array(specs["a51"], params["a51"], r2_0, r2_0 + 4)
+    assert got.size == meta["count"]
+    assert got[:64].tolist() == meta["first"] and got[-64:].tolist() == meta["last"]
+    assert u64_digest(got) == meta["digest"]
+
+
+@pytest.mark.skipif(not has_golden("prune.json"), reason="prune fixture not generated")
+@pytest.mark.parametrize("name", ["mini567", "mini789"])
+def test_prune_minis(gpu, lc, specs, params, name):
+    fx = golden_json("prune.json")
+    cands = list(lc.enumerate_candidates(specs[name], params[name]))
+    for key, want in fx.items():
+        if not key.startswith(name + "_") or key.endswith("_probe"):
+            continue
+        _, mode, lim = key.split("_")
+        cfg = lc.PruneConfig(mode=mode, depth_limit=int(lim) if mode == "dfs" else None,
+                             node_limit=int(lim) if mode == "bfs" else None)
+        surv, st = lc.prune_shallow_segments(cands, cfg, specs[name], params[name])
+        assert u64_digest(surv) == want["survivors_digest"], key
+        assert (st.total, st.removed, st.expanded) == (want["total"], want["removed"], want["expanded"]), key
+
+
+@pytest.mark.skipif(not has_golden("prune.json"), reason="prune fixture not generated")
+def test_prune_a51_sample(gpu, lc, specs, params):
+    fx = golden_json("prune.json")
+    cands = fx["a51_cands"]
+    for key, want in fx.items():
+        if not key.startswith("a51_") or key == "a51_cands":
+            continue
+        _, mode, lim = key.split("_")
+        cfg = lc.PruneConfig(mode=mode, depth_limit=int(lim) if mode == "dfs" else None,
+                             node_limit=int(lim) if mode == "bfs" else None)
+        surv, st = lc.prune_shallow_segments(cands, cfg, specs["a51"], params["a51"])
+        assert surv == want["survivors"], key
+        assert (st.total, st.removed, st.expanded) == (want["total"], want["removed"], want["expanded"]), key
+        if "per_candidate" in want:
+            from paper_1210_6411_b200 import _batch
+
+            removed, work = _batch.prune(cands, specs["a51"], params["a51"], mode, int(lim))
+            assert [[int(r), int(w)] for r, w in zip(removed, work)] == want["per_candidate"]
+
+
+@pytest.mark.skipif(not has_golden("prune.json"), reason="prune fixture not generated")
+@pytest.mark.parametrize("name", ["mini567", "mini789"])
+def test_probe_segment_minis(gpu, lc, specs, params, name):
+    probes = golden_json("prune.json")[f"{name}_probe"]
+    cands = list(lc.enumerate_candidates(specs[name], params[name]))[:64]
+    for x, (depth, nodes, cens, levels) in zip(cands, probes):
+        lc_ = []
+        got = lc.probe_segment(x, specs[name], params[name], level_counts=lc_)
+        assert got == (depth, nodes, cens)
+        assert lc_ == levels
+
+
+@pytest.mark.parametrize("name", ["mini567", "mini789"])
+def test_build_skeleton_edges_closed_set(gpu, lc, specs, params, name):
+    g = golden_npz(f"edges_{name}")
+    edges = lc.build_skeleton_edges(g["src"].tolist(), params[name], specs[name])
+    assert [e.destination for e in edges] == g["dst"].tolist()
+    assert [e.distance for e in edges] == g["dist"].tolist()
+    assert all(e.subtree_size == 0 and e.subtree_depth == 0 for e in edges)
+
+
+def test_build_skeleton_edges_detects_unsound_prune(gpu, lc, specs, params):
+    g = golden_npz("edges_mini567")
+    with pytest.raises(lc.PruneSoundnessError):
+        lc.build_skeleton_edges(g["src"][:100].tolist(), params["mini567"], specs["mini567"])
+    with pytest.raises(ValueError):
+        lc.build_skeleton_edges([], params["mini567"], specs["mini567"])
+
+
+@pytest.mark.parametrize("name", ["a51", "mini789"])
+def test_k0_matches_numpy_restatement(gpu, lc, specs, params, name):
+    from oracle import k0
+
+    got = lc.random_candidates_gpu(specs[name], params[name], seed=12345, n=5000)
+    want = k0.random_candidates(specs[name], params[name].fixed_r3, 12345, 5000)
+    assert (got == want).all()
+    assert lc.is_candidate(got, params[name], specs[name]).all()

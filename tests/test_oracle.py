@@ -1,0 +1,131 @@
+"""Pins the C oracle (oracle/lfsr_oracle.c) to the reference: every fixture here was
+produced by the unmodified reference (oracle/gen_golden.py).  CPU only."""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden_json, golden_npz, has_golden
+
+from oracle import port
+
+
+def edge_digest(src, dst, dist):
+    rows = sorted(zip((int(s) for s in src), (int(d) for d in dst), (int(w) for w in dist)))
+    h = hashlib.sha256()
+    for s, d, w in rows:
+        h.update(f"{s:016x} {d:016x} {w}\n".encode())
+    return h.hexdigest()
+
+
+def u64_digest(values):
+    return hashlib.sha256(np.asarray(values, dtype="<u8").tobytes()).hexdigest()
+
+
+def test_table_matches_reference():
+    t = golden_json("tables.json")
+    assert [list(e) for e in port.table_entries()] == t["entries"]
+    assert t["nonempty_mask"] == "0xb5bf5d0db0bafdad"
+
+
+@pytest.mark.parametrize("name", ["a51", "mini567", "mini789"])
+def test_trajectories(specs, name):
+    g = golden_npz(f"traj_{name}")
+    assert (port.clock_n(specs[name], g["starts"], 1) == g["traj"][:, 0]).all()
+    assert (port.clock_n(specs[name], g["starts"], 64) == g["traj"][:, 63]).all()
+    assert (port.clock_sliced(specs[name], g["starts"], 500) == g["after500"]).all()
+
+
+@pytest.mark.parametrize("name", ["a51", "mini567", "mini789"])
+def test_predicate_and_predecessors(specs, params, name):
+    g = golden_npz(f"pred_{name}")
+    F = params[name].fixed_r3
+    for i in range(0, g["states"].size, 3):
+        x = int(g["states"][i])
+        ps = port.predecessors(specs[name], x)
+        assert len(ps) == g["npred"][i]
+        assert ps == [int(v) for v in g["preds"][i][: len(ps)]]
+        assert port.is_candidate(specs[name], F, x) == bool(g["is_candidate"][i])
+        assert port.table_index(specs[name], x) == g["table_index"][i]
+
+
+@pytest.mark.parametrize("name", ["mini567", "mini789"])
+def test_mini_edges_and_strides(specs, params, name):
+    spec, F = specs[name], params[name].fixed_r3
+    g = golden_npz(f"edges_{name}")
+    meta = golden_json(f"edges_{name}.json")
+    cands = port.enumerate_rows(spec, F, 1, 1 << spec.lengths[1])
+    assert (cands == g["src"]).all()
+    d, w = port.walk(spec, F, cands)
+    assert edge_digest(cands, d[:, 0], w[:, 0]) == meta["digest"]
+    d, w = port.walk(spec, F, g["random_starts"])
+    assert (d[:, 0] == g["random_dst"]).all() and (w[:, 0] == g["random_dist"]).all()
+    for s in (16, 100, 127, 148, 149, 150, 200):
+        d, w = port.walk(spec, F, cands, stride=s)
+        assert (d[:, 0] == g[f"stride_{s}_dst"]).all() and (w[:, 0] == g[f"stride_{s}_dist"]).all()
+    d, w = port.walk(spec, F, g["hop_starts"], legs=2)
+    assert (np.stack([d[:, 0], w[:, 0], d[:, 1], w[:, 1]], 1) == g["hop2"]).all()
+
+
+def test_cap_band_reproduces_reference_quirks(specs, params):
+    cap = golden_json("cap_mini567.json")
+    for mc, outcome in cap["band"].items():
+        try:
+            d, w = port.walk(specs["mini567"], 0x22, [cap["first_candidate"]], max_clocks=int(mc))
+            got = ["ok", int(d[0, 0]), int(w[0, 0])]
+        except port.OracleStrideError:
+            got = ["StrideError"]
+        except port.OracleValueError:
+            got = ["ValueError"]
+        assert got == outcome[: len(got)]
+    with pytest.raises(port.OracleStrideError):
+        port.walk(specs["mini567"], 0x22, cap["cap3_starts"], max_clocks=3)
+
+
+def test_a51_kat(specs, params):
+    g = golden_npz("a51_kat256")
+    meta = golden_json("a51_kat256.json")
+    d, w = port.walk(specs["a51"], 0x2AAA00, g["src"], stride=11_170_000)
+    assert (d[:, 0] == g["dst"]).all() and (w[:, 0] == g["dist"]).all()
+    assert edge_digest(g["src"], d[:, 0], w[:, 0]) == meta["digest"]
+
+
+def test_enumerate_rows_a51():
+    meta = golden_json("enumerate.json")
+    import paper_1210_6411_b200 as lc
+
+    got = port.enumerate_rows(lc.A51, 0x2AAA00, 0x1234, 0x1234 + 4)
+    want = meta["a51_rows_0x1234_4"]
+    assert got.size == want["count"] and u64_digest(got) == want["digest"]
+
+
+@pytest.mark.skipif(not has_golden("prune.json"), reason="prune fixture not generated")
+def test_prune_matches_reference(specs, params):
+    fx = golden_json("prune.json")
+    cands = np.array(fx["a51_cands"], dtype=np.uint64)
+    for key in ("a51_dfs_56", "a51_dfs_319", "a51_bfs_1000"):
+        _, mode, lim = key.split("_")
+        removed, work = port.prune(specs["a51"], 0x2AAA00, mode, int(lim), cands)
+        want = fx[key]
+        assert cands[removed == 0].tolist() == want["survivors"]
+        assert int(work.sum()) == want["expanded"]
+    for name in ("mini567", "mini789"):
+        spec, F = specs[name], params[name].fixed_r3
+        mc = port.enumerate_rows(spec, F, 1, 1 << spec.lengths[1])
+        for key, want in fx.items():
+            if key.startswith(name + "_") and not key.endswith("probe"):
+                _, mode, lim = key.split("_")
+                removed, work = port.prune(spec, F, mode, int(lim), mc)
+                assert u64_digest(mc[removed == 0]) == want["survivors_digest"]
+                assert int(work.sum()) == want["expanded"]
+
+
+@pytest.mark.skipif(not has_golden("a51_c1_65536.json"), reason="C1 fixture not generated")
+def test_c1_sample_rows(specs):
+    """Spot rows of the full 2^16 config-1 reference run (every 256th walk)."""
+    g = golden_npz("a51_c1_sample")
+    d, w = port.walk(specs["a51"], 0x2AAA00, g["src"], stride=11_170_000)
+    assert (d[:, 0] == g["dst"]).all() and (w[:, 0] == g["dist"]).all()
