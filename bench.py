@@ -172,7 +172,8 @@ def main() -> None:
     ctx = N.context(local)
     sspec = N.spec_struct(spec)
     dev = torch.device("cuda", local)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)  # explicit stream: kernels and events share it
+    torch.cuda.set_stream(stream)
 
     per_gpu = 1 << args.workload_log2
     batch = 1 << args.batch_log2

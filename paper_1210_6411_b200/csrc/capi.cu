@@ -115,8 +115,35 @@ struct lc_ctx {
   int device = 0;
   int sms = 0;
   cudaStream_t stream = nullptr;
-  DevBuf meta, queue, stats, a, b, c, d, scratch;
+  DevBuf meta, queue, stats, a, b, c, d, scratch, smmap;
+  int mapped_sms = -1;  // SMs found by the %smid probe (-1: not probed yet)
 };
+
+namespace {
+
+// Dense index for every %smid of the device, so the walk can keep one queue per warp
+// scheduler (4 per SM).  Probed once per context.
+int ensure_smsp_map(lc_ctx* ctx) {
+  if (ctx->mapped_sms >= 0) return LC_OK;
+  LC_CUDA(ctx->smmap.ensure(1024 * sizeof(unsigned int) + 1024 * sizeof(uint16_t)));
+  unsigned int* flags = ctx->smmap.as<unsigned int>();
+  LC_CUDA(cudaMemsetAsync(flags, 0, 1024 * sizeof(unsigned int), ctx->stream));
+  LC_CUDA(lc::probe_smids(ctx->sms, flags, ctx->stream));
+  g_launches += 1;
+  unsigned int h[1024];
+  LC_CUDA(cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  LC_CUDA(cudaStreamSynchronize(ctx->stream));
+  uint16_t map[1024];
+  int k = 0;
+  for (int i = 0; i < 1024; ++i) map[i] = h[i] ? static_cast<uint16_t>(k++) : 0;
+  uint16_t* dmap = reinterpret_cast<uint16_t*>(flags + 1024);
+  LC_CUDA(cudaMemcpyAsync(dmap, map, sizeof(map), cudaMemcpyHostToDevice, ctx->stream));
+  LC_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->mapped_sms = k;
+  return LC_OK;
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -154,7 +181,7 @@ int lc_ctx_destroy(lc_ctx* ctx) {
   if (!ctx) return LC_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  for (DevBuf* b : {&ctx->meta, &ctx->queue, &ctx->stats, &ctx->a, &ctx->b, &ctx->c, &ctx->d, &ctx->scratch})
+  for (DevBuf* b : {&ctx->meta, &ctx->queue, &ctx->stats, &ctx->a, &ctx->b, &ctx->c, &ctx->d, &ctx->scratch, &ctx->smmap})
     b->release();
   cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -209,13 +236,8 @@ int lc_walk_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const ui
   if (refill > 1024) return fail(LC_ERR_ARG, "refill must be in [0, 1024]");
   if (!d_stats) return fail(LC_ERR_ARG, "stats buffer required");
   LC_CUDA(cudaSetDevice(ctx->device));
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-
-  // stats header: counters zero, min = ~0, error index = ~0, histogram config
-  LC_CUDA(lc::launch_init_stats(d_stats, hist_lo, hist_shift, hist_bins, st));
-  g_launches += 1;
-  if (n == 0) return LC_OK;
-  if (!d_starts || !d_dest || !d_dist) return fail(LC_ERR_ARG, "null buffer");
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  if ((rc = ensure_smsp_map(ctx))) return rc;
 
   const bool static_f = fixed_r3 == default_fixed(id);
   const int per_sm = lc::walk_blocks_per_sm(id, static_f);
@@ -225,10 +247,20 @@ int lc_walk_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const ui
   const int blocks = static_cast<int>(std::max<uint64_t>(1, std::min(max_blocks, want)));
   uint32_t refill_min = refill;
   if (refill_min == 0) refill_min = (legs == 1 && stride > 1) ? 1024u : 1u;
+  // one queue per warp scheduler when the persistent grid covers every SM
+  const uint32_t nq = (ctx->mapped_sms == ctx->sms && static_cast<uint64_t>(blocks) == max_blocks)
+                          ? 4u * static_cast<uint32_t>(ctx->sms) : 1u;
 
   LC_CUDA(ctx->meta.ensure(static_cast<size_t>(blocks) * lanes_per_block * sizeof(lc::LaneMeta)));
-  LC_CUDA(ctx->queue.ensure(sizeof(unsigned long long)));
-  LC_CUDA(cudaMemsetAsync(ctx->queue.p, 0, sizeof(unsigned long long), st));
+  LC_CUDA(ctx->queue.ensure((static_cast<size_t>(nq) * 16 + 16) * sizeof(unsigned long long)));
+  unsigned long long* queues = ctx->queue.as<unsigned long long>();
+  unsigned int* exhausted = reinterpret_cast<unsigned int*>(queues + static_cast<size_t>(nq) * 16);
+
+  // stats header (counters zero, min = ~0, error index = ~0, histogram config), queues
+  LC_CUDA(lc::launch_init_stats(d_stats, hist_lo, hist_shift, hist_bins, queues, nq, exhausted, st));
+  g_launches += 1;
+  if (n == 0) return LC_OK;
+  if (!d_starts || !d_dest || !d_dist) return fail(LC_ERR_ARG, "null buffer");
 
   lc::WalkParams p{};
   p.starts = d_starts;
@@ -243,7 +275,11 @@ int lc_walk_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const ui
   p.legs = legs;
   p.fixed_r3 = static_cast<uint32_t>(fixed_r3);
   p.refill_min = refill_min;
-  p.queue = ctx->queue.as<unsigned long long>();
+  p.chunk = refill_min >= 1024u ? 1024u : 1u;
+  p.nq = nq;
+  p.queues = queues;
+  p.smsp_map = reinterpret_cast<const uint16_t*>(ctx->smmap.as<unsigned int>() + 1024);
+  p.exhausted = exhausted;
   p.stats = reinterpret_cast<unsigned long long*>(d_stats);
   p.meta = ctx->meta.as<lc::LaneMeta>();
   LC_CUDA(lc::launch_walk(id, static_f, p, blocks, st));

@@ -35,28 +35,53 @@ using MINI789 = Spec<7, 8, 9, (1u << 5) | (1u << 6), (1u << 3) | (1u << 4) | (1u
 
 // ------------------------------------------------------------------ bitsliced clock
 
+// Explicit LOP3s (PTX lop3.b32) so the step compiles to exactly the hand count.
+// Immediates use the PTX convention a = 0xF0, b = 0xCC, c = 0xAA.
+template <uint32_t IMM>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(IMM));
+  return d;
+}
+// e ? a : b  =  (e & a) | (~e & b)
+__device__ __forceinline__ uint32_t mux(uint32_t e, uint32_t a, uint32_t b) { return lop3<0xCA>(e, a, b); }
+__device__ __forceinline__ uint32_t xor3(uint32_t a, uint32_t b, uint32_t c) { return lop3<0x96>(a, b, c); }
+
+// Register k is clocked iff its clock bit equals the majority, i.e. it agrees with at
+// least one of the other two: e_k = ~((c_k ^ c_i) & (c_k ^ c_j)) -- one LOP3 (0xE7).
+__device__ __forceinline__ uint32_t clock_enable(uint32_t ck, uint32_t ci, uint32_t cj) {
+  return lop3<0xE7>(ck, ci, cj);
+}
+
+// Bit 0 of a clocked register receives the XOR of its taps: r0' = e ? xor(taps) : r0.
+// Taps are folded three at a time; the last fold is fused with the insert when at
+// most one tap remains (2 taps: x = t0^t1^r0, r0' = r0 ^ (e & x) -- 2 LOP3).
 template <uint32_t TM, int L, int OFF, int NB>
-__device__ __forceinline__ uint32_t feedback(const uint32_t (&s)[NB]) {
-  uint32_t f = 0;
+__device__ __forceinline__ uint32_t feedback_insert(const uint32_t (&s)[NB], uint32_t e) {
+  constexpr int n = __builtin_popcount(TM);
+  uint32_t t[4] = {0, 0, 0, 0};
+  int k = 0;
 #pragma unroll
   for (int i = 0; i < L; ++i)
-    if ((TM >> i) & 1u) f ^= s[OFF + i];
-  return f;
+    if ((TM >> i) & 1u) t[k++ & 3] = s[OFF + i];
+  const uint32_t r0 = s[OFF];
+  if constexpr (n == 2) {
+    return lop3<0x78>(r0, e, xor3(t[0], t[1], r0));  // r0 ^ (e & (t0 ^ t1 ^ r0))
+  } else if constexpr (n == 3) {
+    return mux(e, xor3(t[0], t[1], t[2]), r0);
+  } else {
+    static_assert(n == 4, "tap count");
+    return mux(e, lop3<0x3C>(xor3(t[0], t[1], t[2]), t[3], 0u), r0);  // 0x3C: a ^ b
+  }
 }
 
 // Conditional shift of one register: lanes with e set take r[i-1] (and the feedback
 // at bit 0), the others keep r[i].  One LOP3 per bit.
 template <int L, int OFF, int NB>
-__device__ __forceinline__ void cond_shift(uint32_t (&s)[NB], uint32_t e, uint32_t f) {
+__device__ __forceinline__ void cond_shift(uint32_t (&s)[NB], uint32_t e, uint32_t r0_new) {
 #pragma unroll
-  for (int i = L - 1; i > 0; --i) s[OFF + i] = (s[OFF + i - 1] & e) | (s[OFF + i] & ~e);
-  s[OFF] = (f & e) | (s[OFF] & ~e);
-}
-
-// Register k is clocked iff its clock bit equals the majority, i.e. it agrees with at
-// least one of the other two: e_k = ~((c_k ^ c_i) & (c_k ^ c_j)) -- one LOP3.
-__device__ __forceinline__ uint32_t clock_enable(uint32_t ck, uint32_t ci, uint32_t cj) {
-  return ~((ck ^ ci) & (ck ^ cj));
+  for (int i = L - 1; i > 0; --i) s[OFF + i] = mux(e, s[OFF + i - 1], s[OFF + i]);
+  s[OFF] = r0_new;
 }
 
 // One majority-clocked step of 32 lanes (cipher.py:228-253 / bitslice.py:131-157):
@@ -68,12 +93,12 @@ __device__ __forceinline__ void step(uint32_t (&s)[S::NB]) {
   const uint32_t e1 = clock_enable(c1, c2, c3);
   const uint32_t e2 = clock_enable(c2, c1, c3);
   const uint32_t e3 = clock_enable(c3, c1, c2);
-  const uint32_t f1 = feedback<S::T1, S::L1, 0>(s);
-  const uint32_t f2 = feedback<S::T2, S::L2, S::O2>(s);
-  const uint32_t f3 = feedback<S::T3, S::L3, S::O3>(s);
-  cond_shift<S::L1, 0>(s, e1, f1);
-  cond_shift<S::L2, S::O2>(s, e2, f2);
-  cond_shift<S::L3, S::O3>(s, e3, f3);
+  const uint32_t n1 = feedback_insert<S::T1, S::L1, 0>(s, e1);
+  const uint32_t n2 = feedback_insert<S::T2, S::L2, S::O2>(s, e2);
+  const uint32_t n3 = feedback_insert<S::T3, S::L3, S::O3>(s, e3);
+  cond_shift<S::L1, 0>(s, e1, n1);
+  cond_shift<S::L2, S::O2>(s, e2, n2);
+  cond_shift<S::L3, S::O3>(s, e3, n3);
 }
 
 // Lanes whose R3 equals the fixed value (bitslice.py:195-209 match_mask) -- an AND of

@@ -35,11 +35,15 @@ struct WalkParams {
   uint32_t hist_bins;
   uint32_t legs;
   uint32_t fixed_r3;
-  uint32_t refill_min;  // refill once this many of the warp's 1024 lanes are idle
+  uint32_t refill_min;  // lane mode: refill once this many of the warp's 1024 lanes are idle
+  uint32_t chunk;       // starts per queue item: 1024 (whole-warp refill) or 1 (lane refill)
+  uint32_t nq;          // queues: one per SM sub-partition, or 1
   uint32_t pad;
-  unsigned long long* queue;  // next start index
-  unsigned long long* stats;  // LC_ST_* block
-  LaneMeta* meta;             // [threads][32]
+  unsigned long long* queues;  // nq counters, 16 words apart
+  const uint16_t* smsp_map;    // %smid -> dense SM index (nq > 1)
+  unsigned int* exhausted;     // set once every queue is empty
+  unsigned long long* stats;   // LC_ST_* block
+  LaneMeta* meta;              // [threads][32]
 };
 
 // Launchers (defined in the .cu files); all enqueue on `stream`.
@@ -47,7 +51,9 @@ cudaError_t launch_walk(SpecId id, bool static_f, const WalkParams& p, int block
                         cudaStream_t stream);
 int walk_blocks_per_sm(SpecId id, bool static_f);
 cudaError_t launch_init_stats(uint64_t* stats, uint64_t hist_lo, uint32_t hist_shift, uint32_t hist_bins,
+                              unsigned long long* queues, uint32_t nq, unsigned int* exhausted,
                               cudaStream_t stream);
+cudaError_t probe_smids(int sms, unsigned int* d_flags, cudaStream_t stream);
 
 cudaError_t launch_is_candidate(SpecId id, const uint64_t* xs, uint64_t n, uint32_t F, uint8_t* out,
                                 cudaStream_t stream);

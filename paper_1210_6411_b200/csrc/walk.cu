@@ -10,9 +10,16 @@
 //    hop 1 (bitslice.py:291-293), and never before 2^l3-1 clocks after starting on a
 //    candidate (no R3 return earlier -- SURVEY.md A.3), so the mask is evaluated on a
 //    small fraction of steps;
-//  * finished lanes are refilled from a global queue: warp ballot/popc prefix, one
-//    atomicAdd per warp, per-lane insertion -- results go to the start's own slot, so the
-//    output order is the input order regardless of scheduling;
+//  * per-thread control state lives in (volatile) shared memory, so only the 64 state
+//    words and the step temporaries are live in the hot loops (which compile to exactly
+//    72 LOP3 per step with the loop control on the uniform datapath; 20 warps per SM);
+//  * work is handed out from one queue per SM sub-partition (warp scheduler): item i
+//    belongs to queue i mod Q, so every scheduler ends with the same amount of work to
+//    within one item, and warps steal from other queues once their own is empty;
+//  * a warp refills either all 1024 lanes at once from one 1024-start item (warp ballot
+//    32x32 transposes of coalesced loads) or single idle lanes (ballot / popc prefix /
+//    one atomic per warp) -- results go to the start's own slot, so the output order is
+//    the input order regardless of scheduling;
 //  * the per-leg cap audit reproduces the reference's StrideError condition exactly
 //    (DESIGN.md "Cap").
 #include <cuda_runtime.h>
@@ -28,6 +35,11 @@ namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kChunk = 1u << 20;  // max steps between control points (abort polling)
+constexpr int kQueueStride = 16;       // u64 words between queue counters (128 B)
+
+#ifndef LC_WALK_MIN_BLOCKS
+#define LC_WALK_MIN_BLOCKS 5  // 5 x 128 threads: 20 warps/SM -> <= 102 registers, spill-free hot loops
+#endif
 
 __device__ __forceinline__ uint64_t sat_add(uint64_t a, uint64_t b) {
   const uint64_t c = a + b;
@@ -88,166 +100,364 @@ __device__ __forceinline__ uint32_t run_checked(uint32_t (&s)[S::NB], uint32_t n
   return k;
 }
 
+// Warp-uniform view of the error word.
+__device__ __forceinline__ bool raise_pending(const WalkParams& p) {
+  const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&p.stats[LC_ST_ERROR]);
+  return __shfl_sync(kFull, e, 0) != 0ull;
+}
+
+// Items in queue q (items i with i mod nq == q).
+__device__ __forceinline__ uint64_t queue_len(uint64_t items, uint32_t nq, uint32_t q) {
+  return items > q ? (items - q + nq - 1) / nq : 0;
+}
+
+// Take up to m items, own queue first, then steal.  Lane 0 only.  Returns the count;
+// the items are (base + j) * nq + qi for j < count.
+__device__ uint32_t take_items(const WalkParams& p, uint64_t items, uint32_t own, uint32_t m,
+                               uint32_t* qi_out, uint64_t* base_out) {
+  for (uint32_t i = 0; i < p.nq; ++i) {
+    const uint32_t qi = own + i < p.nq ? own + i : own + i - p.nq;
+    const uint64_t len = queue_len(items, p.nq, qi);
+    unsigned long long* ctr = p.queues + static_cast<uint64_t>(qi) * kQueueStride;
+    if (i != 0) {
+      if (*reinterpret_cast<volatile unsigned int*>(p.exhausted)) break;
+      if (*reinterpret_cast<volatile unsigned long long*>(ctr) >= len) continue;
+    }
+    const uint64_t b = atomicAdd(ctr, static_cast<unsigned long long>(m));
+    if (b < len) {
+      *qi_out = qi;
+      *base_out = b;
+      return static_cast<uint32_t>(len - b < m ? len - b : m);
+    }
+  }
+  atomicExch(p.exhausted, 1u);
+  return 0;
+}
+
+// Special registers read with asm volatile so the compiler re-reads them after the hot
+// loops instead of keeping copies live across them.
+__device__ __forceinline__ uint32_t tid_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t ctaid_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(r));
+  return r;
+}
+
+// Per-block control state in shared memory.  Everything the outer loop needs after a
+// hot loop is re-read from here, so only the 64 state words (plus the uniform step
+// counter) are live in the hot loops.
+struct WalkShared {
+  uint32_t active[kWalkThreads];            // lanes walking
+  uint32_t armed[kWalkThreads];             // lanes allowed to report a special node
+  unsigned long long next_arm[kWalkThreads];
+  unsigned long long next_dead[kWalkThreads];
+  unsigned long long t[kWalkThreads / 32];  // warp clock
+  uint32_t own[kWalkThreads / 32];          // warp scheduler queue
+  uint32_t open[kWalkThreads / 32];         // queues not yet exhausted for this warp
+};
+
 template <class S, bool SF>
-__global__ void __launch_bounds__(kWalkThreads) walk_kernel(const WalkParams p) {
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  LaneMeta* meta = p.meta + gtid * 32u;
+__device__ __forceinline__ void whole_warp_refill(const WalkParams& p, volatile WalkShared& sh,
+                                                  uint32_t (&s)[S::NB]) {
   constexpr uint64_t kStateMask = S::NB >= 64 ? ~0ull : ((1ull << S::NB) - 1ull);
+  const uint32_t tid = tid_x(), lane = tid & 31u, w = tid >> 5;
+  const uint64_t gtid = static_cast<uint64_t>(ctaid_x()) * kWalkThreads + tid;
+  const uint64_t items = (p.n + p.chunk - 1) / p.chunk;
+  const uint64_t t = sh.t[w];
+  uint32_t qi = 0, got = 0;
+  uint64_t b = 0;
+  if (lane == 0) got = take_items(p, items, sh.own[w], 1u, &qi, &b);
+  got = __shfl_sync(kFull, got, 0);
+  if (got == 0u) {
+    if (lane == 0) sh.open[w] = 0u;
+    __syncwarp();
+    return;
+  }
+  qi = __shfl_sync(kFull, qi, 0);
+  b = __shfl_sync(kFull, b, 0);
+  const uint64_t base = ((b * p.nq) + qi) * p.chunk;
+  const uint64_t wbase = gtid - lane;  // first thread of this warp
+  bool all_safe = true;
+  for (uint32_t r = 0; r < 32u; ++r) {
+    const uint64_t k = base + r * 32u + lane;
+    uint64_t x = 0;
+    bool valid = false;
+    if (k < p.n) {
+      x = p.starts[k] & kStateMask;  // transpose keeps nbits (bitslice.py:66-78)
+      const uint32_t r1 = static_cast<uint32_t>(x & S::M1);
+      const uint32_t r2 = static_cast<uint32_t>((x >> S::O2) & S::M2);
+      const uint32_t r3 = static_cast<uint32_t>((x >> S::O3) & S::M3);
+      if (r1 == 0u || r2 == 0u || r3 == 0u) {
+        raise_error(p.stats, LC_ERR_INVALID_STATE, k);
+        x = 0;
+      } else {
+        valid = true;
+        const uint32_t c1 = (r1 >> S::CT1) & 1u, c2 = (r2 >> S::CT2) & 1u, c3 = (r3 >> S::CT3) & 1u;
+        all_safe = all_safe && r3 == p.fixed_r3 && (c3 == c1 || c3 == c2);
+        LaneMeta m;
+        m.walk = k;
+        m.leg_start = t;
+        m.arm_at = 0;    // set by the owning thread below
+        m.deadline = 0;  // (identical for every lane of the item)
+        m.legs_done = 0u;
+        m.pad = 0u;
+        p.meta[(wbase + r) * 32u + lane] = m;
+      }
+    }
+    const uint32_t vmask = __ballot_sync(kFull, valid);
+    const uint32_t lo = static_cast<uint32_t>(x), hi = static_cast<uint32_t>(x >> 32);
+#pragma unroll
+    for (int i = 0; i < S::NB; ++i) {
+      const uint32_t wd = __ballot_sync(kFull, ((i < 32 ? lo >> i : hi >> (i - 32)) & 1u) != 0u);
+      if (lane == r) s[i] = wd;
+    }
+    if (lane == r) sh.active[tid] = vmask;
+  }
+  // a start on the fixed plane whose R3 is clocked at once cannot meet R3 == F again
+  // for 2^l3 - 1 clocks
+  all_safe = __all_sync(kFull, all_safe);
+  const uint64_t first = max(p.stride, static_cast<uint64_t>(all_safe ? S::WINDOW : 1ull));
+  const uint64_t arm = sat_add(t, first), dead = sat_add(t, max(p.stride, p.cap1));
+  __syncwarp();
+  LaneMeta* const meta = p.meta + gtid * 32u;
+  const uint32_t act = sh.active[tid];
+  for (uint32_t a = act; a != 0u; a &= a - 1u) {
+    const int j = __ffs(a) - 1;
+    meta[j].arm_at = arm;
+    meta[j].deadline = dead;
+  }
+  sh.armed[tid] = 0u;
+  sh.next_arm[tid] = act ? arm : kInf;
+  sh.next_dead[tid] = act ? dead : kInf;
+  __syncwarp();
+}
+
+template <class S, bool SF>
+__device__ __forceinline__ void lane_refill(const WalkParams& p, volatile WalkShared& sh,
+                                            uint32_t (&s)[S::NB]) {
+  constexpr uint64_t kStateMask = S::NB >= 64 ? ~0ull : ((1ull << S::NB) - 1ull);
+  const uint32_t tid = tid_x(), lane = tid & 31u, w = tid >> 5;
+  const uint64_t gtid = static_cast<uint64_t>(ctaid_x()) * kWalkThreads + tid;
+  LaneMeta* const meta = p.meta + gtid * 32u;
+  const uint64_t items = p.n;  // chunk == 1: item == start index
+  const uint64_t t = sh.t[w];
+  for (;;) {
+    const uint32_t idle = ~sh.active[tid];
+    const uint32_t nidle = __popc(idle);
+    const uint32_t widle = __reduce_add_sync(kFull, nidle);
+    if (widle == 0u || widle < p.refill_min) break;
+    uint32_t qi = 0, got = 0;
+    uint64_t b = 0;
+    if (lane == 0) got = take_items(p, items, sh.own[w], widle, &qi, &b);
+    got = __shfl_sync(kFull, got, 0);
+    if (got == 0u) {
+      if (lane == 0) sh.open[w] = 0u;
+      __syncwarp();
+      break;
+    }
+    qi = __shfl_sync(kFull, qi, 0);
+    b = __shfl_sync(kFull, b, 0);
+    uint32_t incl = nidle;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(kFull, incl, o);
+      if (lane >= static_cast<uint32_t>(o)) incl += v;
+    }
+    uint32_t j_item = incl - nidle;  // this thread's first item offset
+    uint32_t active = sh.active[tid];
+    uint64_t next_arm = sh.next_arm[tid], next_dead = sh.next_dead[tid];
+    for (uint32_t todo = idle; todo != 0u && j_item < got; todo &= todo - 1u, ++j_item) {
+      const int j = __ffs(todo) - 1;
+      const uint64_t k = (b + j_item) * p.nq + qi;
+      const uint64_t x = p.starts[k] & kStateMask;
+      const uint32_t r1 = static_cast<uint32_t>(x & S::M1);
+      const uint32_t r2 = static_cast<uint32_t>((x >> S::O2) & S::M2);
+      const uint32_t r3 = static_cast<uint32_t>((x >> S::O3) & S::M3);
+      if (r1 == 0u || r2 == 0u || r3 == 0u) {
+        raise_error(p.stats, LC_ERR_INVALID_STATE, k);
+        continue;
+      }
+      insert_lane<S::NB>(s, j, x);
+      const uint32_t c1 = (r1 >> S::CT1) & 1u, c2 = (r2 >> S::CT2) & 1u, c3 = (r3 >> S::CT3) & 1u;
+      const bool safe = r3 == p.fixed_r3 && (c3 == c1 || c3 == c2);
+      LaneMeta m;
+      m.walk = k;
+      m.leg_start = t;
+      m.arm_at = sat_add(t, max(p.stride, static_cast<uint64_t>(safe ? S::WINDOW : 1ull)));
+      m.deadline = sat_add(t, max(p.stride, p.cap1));
+      m.legs_done = 0u;
+      m.pad = 0u;
+      meta[j] = m;
+      active |= 1u << j;
+      next_arm = min(next_arm, m.arm_at);
+      next_dead = min(next_dead, m.deadline);
+    }
+    sh.active[tid] = active;
+    sh.next_arm[tid] = next_arm;
+    sh.next_dead[tid] = next_dead;
+    if (raise_pending(p)) break;
+  }
+}
+
+// Events at the warp clock (rare): special nodes, arming, cap audits.
+template <class S, bool SF>
+__device__ __forceinline__ void handle_events(const WalkParams& p, volatile WalkShared& sh,
+                                              const uint32_t (&s)[S::NB]) {
+  const uint32_t tid = tid_x(), w = tid >> 5;
+  const uint64_t gtid = static_cast<uint64_t>(ctaid_x()) * kWalkThreads + tid;
+  LaneMeta* const meta = p.meta + gtid * 32u;
+  const uint64_t t = sh.t[w];
+  const uint32_t F = p.fixed_r3;
+  uint32_t active = sh.active[tid], armed = sh.armed[tid];
+  uint64_t next_arm = sh.next_arm[tid], next_dead = sh.next_dead[tid];
+  uint32_t hits = special_mask<S, SF>(s, F) & armed;
+  if (hits != 0u) {
+    while (hits != 0u) {
+      const int j = __ffs(hits) - 1;
+      hits &= hits - 1u;
+      const uint32_t bit = 1u << j;
+      LaneMeta m = meta[j];
+      const uint64_t d = t - m.leg_start;
+      const uint64_t o = m.walk * p.legs + m.legs_done;
+      p.dst[o] = extract_lane<S::NB>(s, j);
+      p.dist[o] = d;
+      record_edge(p, d);
+      armed &= ~bit;
+      if (++m.legs_done >= p.legs) {
+        active &= ~bit;
+        m.arm_at = kInf;
+        m.deadline = kInf;
+      } else {
+        // the lane continues from the candidate it reached (bitslice.py:313-315)
+        m.leg_start = t;
+        m.arm_at = sat_add(t, S::WINDOW);
+        m.deadline = sat_add(t, p.cap1);
+      }
+      meta[j] = m;
+    }
+    next_arm = kInf;
+    next_dead = kInf;
+    for (uint32_t a = active; a != 0u; a &= a - 1u) {
+      const int j = __ffs(a) - 1;
+      if (!((armed >> j) & 1u)) next_arm = min(next_arm, meta[j].arm_at);
+      next_dead = min(next_dead, meta[j].deadline);
+    }
+  }
+  if (next_arm <= t) {
+    next_arm = kInf;
+    for (uint32_t a = active & ~armed; a != 0u; a &= a - 1u) {
+      const int j = __ffs(a) - 1;
+      const uint64_t at = meta[j].arm_at;
+      if (at <= t) armed |= 1u << j;
+      else next_arm = min(next_arm, at);
+    }
+  }
+  if (next_dead <= t) {
+    // Cap audit: a leg still searching at its deadline raises unless it is inside a run
+    // of fixed-R3 states (whose end is then its special node).
+    const uint32_t on_plane = SF ? match_static<S, S::DEFAULT_F>(s) : match_runtime<S>(s, F);
+    next_dead = kInf;
+    for (uint32_t a = active; a != 0u; a &= a - 1u) {
+      const int j = __ffs(a) - 1;
+      const uint64_t dl = meta[j].deadline;
+      if (dl <= t) {
+        if (!((on_plane >> j) & 1u)) raise_error(p.stats, LC_ERR_CAP, meta[j].walk);
+        meta[j].deadline = kInf;
+      } else {
+        next_dead = min(next_dead, dl);
+      }
+    }
+  }
+  sh.active[tid] = active;
+  sh.armed[tid] = armed;
+  sh.next_arm[tid] = next_arm;
+  sh.next_dead[tid] = next_dead;
+}
+
+template <class S, bool SF>
+__global__ void __launch_bounds__(kWalkThreads, LC_WALK_MIN_BLOCKS) walk_kernel(const WalkParams p) {
+  __shared__ WalkShared sh_storage;
+  volatile WalkShared& sh = sh_storage;
+  {
+    const uint32_t tid = tid_x(), lane = tid & 31u, w = tid >> 5;
+    sh.active[tid] = 0u;
+    sh.armed[tid] = 0u;
+    sh.next_arm[tid] = kInf;
+    sh.next_dead[tid] = kInf;
+    if (lane == 0) {
+      uint32_t own = 0;
+      if (p.nq > 1) {  // this warp's scheduler queue
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        own = (static_cast<uint32_t>(p.smsp_map[smid & 1023u]) * 4u + (w & 3u)) % p.nq;
+      }
+      sh.own[w] = own;
+      sh.t[w] = 0ull;
+      sh.open[w] = 1u;
+    }
+    __syncwarp();
+  }
 
   uint32_t s[S::NB];
 #pragma unroll
   for (int i = 0; i < S::NB; ++i) s[i] = 0u;
-  uint32_t active = 0u, armed = 0u;
-  uint64_t next_arm = kInf, next_dead = kInf;
-  uint64_t t = 0;
-  bool open = true;
 
   for (;;) {
     // ---- abort as soon as any warp has raised (StrideError / invalid start)
-    const unsigned long long err = *reinterpret_cast<volatile unsigned long long*>(&p.stats[LC_ST_ERROR]);
-    if (__shfl_sync(kFull, err, 0) != 0ull) break;
+    if (raise_pending(p)) break;
 
-    // ---- refill idle lanes from the global queue (warp ballot / prefix / one atomic)
-    if (open) {
-      const uint32_t idle = ~active;
-      const uint32_t nidle = __popc(idle);
-      const uint32_t widle = __reduce_add_sync(kFull, nidle);
-      if (widle != 0u && widle >= p.refill_min) {
-        uint32_t incl = nidle;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t v = __shfl_up_sync(kFull, incl, o);
-          if (lane >= static_cast<uint32_t>(o)) incl += v;
-        }
-        unsigned long long base = 0;
-        if (lane == 31u) base = atomicAdd(p.queue, static_cast<unsigned long long>(incl));
-        base = __shfl_sync(kFull, base, 31);
-        if (base + widle >= p.n) open = false;
-        uint64_t k = base + (incl - nidle);
-        uint32_t todo = idle;
-        while (todo != 0u && k < p.n) {
-          const int j = __ffs(todo) - 1;
-          todo &= todo - 1u;
-          const uint64_t x = p.starts[k] & kStateMask;  // transpose keeps nbits (bitslice.py:66-78)
-          const uint32_t r1 = static_cast<uint32_t>(x & S::M1);
-          const uint32_t r2 = static_cast<uint32_t>((x >> S::O2) & S::M2);
-          const uint32_t r3 = static_cast<uint32_t>((x >> S::O3) & S::M3);
-          if (r1 == 0u || r2 == 0u || r3 == 0u) {
-            // SPEC.md:64 contract violation; the reference walks it to the cap
-            raise_error(p.stats, LC_ERR_INVALID_STATE, k);
-            ++k;
-            continue;
-          }
-          insert_lane<S::NB>(s, j, x);
-          // a start on the fixed plane whose R3 is clocked at once cannot meet R3 == F
-          // again for 2^l3 - 1 clocks
-          const uint32_t c1 = (r1 >> S::CT1) & 1u, c2 = (r2 >> S::CT2) & 1u, c3 = (r3 >> S::CT3) & 1u;
-          const bool safe = r3 == p.fixed_r3 && (c3 == c1 || c3 == c2);
-          const uint64_t first = max(p.stride, static_cast<uint64_t>(safe ? S::WINDOW : 1ull));
-          LaneMeta m;
-          m.walk = k;
-          m.leg_start = t;
-          m.arm_at = sat_add(t, first);
-          m.deadline = sat_add(t, max(p.stride, p.cap1));
-          m.legs_done = 0u;
-          m.pad = 0u;
-          meta[j] = m;
-          active |= 1u << j;
-          next_arm = min(next_arm, m.arm_at);
-          next_dead = min(next_dead, m.deadline);
-          ++k;
+    // ---- refill idle lanes
+    uint32_t rel, armed;
+    {
+      const uint32_t tid = tid_x(), w = tid >> 5;
+      if (sh.open[w]) {
+        if (p.chunk > 1u) {
+          if (__all_sync(kFull, sh.active[tid] == 0u)) whole_warp_refill<S, SF>(p, sh, s);
+        } else {
+          lane_refill<S, SF>(p, sh, s);
         }
       }
-    }
-    if (!__any_sync(kFull, active != 0u)) {
-      if (!open) break;
-      continue;
+      if (!__any_sync(kFull, sh.active[tid] != 0u)) {
+        if (!sh.open[w]) break;
+        continue;
+      }
+      // ---- next warp-wide event horizon
+      const uint64_t t = sh.t[w];
+      const uint64_t h = min(sh.next_arm[tid], sh.next_dead[tid]);
+      rel = (h - t) > kChunk ? kChunk : static_cast<uint32_t>(h - t);
+      rel = __reduce_min_sync(kFull, rel);
+      armed = sh.armed[tid];
     }
 
-    // ---- run to the next warp-wide event horizon
-    const uint64_t h = min(next_arm, next_dead);
-    uint32_t rel = (h - t) > kChunk ? kChunk : static_cast<uint32_t>(h - t);
-    rel = __reduce_min_sync(kFull, rel);
-    const bool check = __any_sync(kFull, armed != 0u);
+    // ---- hot loops: only s[], the step count and (checked) the armed mask are live
     uint32_t done;
-    if (check) {
+    if (__any_sync(kFull, armed != 0u)) {
       done = run_checked<S, SF>(s, rel, armed, p.fixed_r3);
     } else {
       run_unchecked<S>(s, rel);
       done = rel;
     }
-    t += done;
-
-    // ---- events at clock t (rare): special nodes, arming, cap audits
-    if (check) {
-      uint32_t hits = special_mask<S, SF>(s, p.fixed_r3) & armed;
-      if (hits != 0u) {
-        while (hits != 0u) {
-          const int j = __ffs(hits) - 1;
-          hits &= hits - 1u;
-          const uint32_t bit = 1u << j;
-          LaneMeta m = meta[j];
-          const uint64_t d = t - m.leg_start;
-          const uint64_t o = m.walk * p.legs + m.legs_done;
-          p.dst[o] = extract_lane<S::NB>(s, j);
-          p.dist[o] = d;
-          record_edge(p, d);
-          armed &= ~bit;
-          if (++m.legs_done >= p.legs) {
-            active &= ~bit;
-            m.arm_at = kInf;
-            m.deadline = kInf;
-          } else {
-            // the lane continues from the candidate it reached (bitslice.py:313-315)
-            m.leg_start = t;
-            m.arm_at = sat_add(t, S::WINDOW);
-            m.deadline = sat_add(t, p.cap1);
-          }
-          meta[j] = m;
-        }
-        next_arm = kInf;
-        next_dead = kInf;
-        for (uint32_t a = active; a != 0u; a &= a - 1u) {
-          const int j = __ffs(a) - 1;
-          if (!((armed >> j) & 1u)) next_arm = min(next_arm, meta[j].arm_at);
-          next_dead = min(next_dead, meta[j].deadline);
-        }
-      }
+    {
+      const uint32_t tid = tid_x(), lane = tid & 31u, w = tid >> 5;
+      __syncwarp();
+      if (lane == 0) sh.t[w] = sh.t[w] + done;
+      __syncwarp();
     }
-    if (next_arm <= t) {
-      next_arm = kInf;
-      for (uint32_t a = active & ~armed; a != 0u; a &= a - 1u) {
-        const int j = __ffs(a) - 1;
-        const uint64_t at = meta[j].arm_at;
-        if (at <= t) armed |= 1u << j;
-        else next_arm = min(next_arm, at);
-      }
-    }
-    if (next_dead <= t) {
-      // Cap audit: a leg still searching at its deadline raises unless it is inside a
-      // run of fixed-R3 states (whose end is then its special node).
-      const uint32_t on_plane = SF ? match_static<S, S::DEFAULT_F>(s) : match_runtime<S>(s, p.fixed_r3);
-      next_dead = kInf;
-      for (uint32_t a = active; a != 0u; a &= a - 1u) {
-        const int j = __ffs(a) - 1;
-        const uint64_t dl = meta[j].deadline;
-        if (dl <= t) {
-          if (!((on_plane >> j) & 1u)) raise_error(p.stats, LC_ERR_CAP, meta[j].walk);
-          meta[j].deadline = kInf;
-        } else {
-          next_dead = min(next_dead, dl);
-        }
-      }
-    }
+    handle_events<S, SF>(p, sh, s);
   }
 }
 
 __global__ void init_stats_kernel(unsigned long long* st, uint64_t hist_lo, uint32_t hist_shift,
-                                  uint32_t hist_bins) {
+                                  uint32_t hist_bins, unsigned long long* queues, uint32_t nq,
+                                  unsigned int* exhausted) {
   const uint64_t words = LC_ST_HEADER + hist_bins + 2ull;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < words;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  for (uint64_t i = i0; i < words; i += stride) {
     unsigned long long v = 0;
     if (i == LC_ST_MIN || i == LC_ST_ERROR_INDEX) v = ~0ull;
     else if (i == LC_ST_HIST_LO) v = hist_lo;
@@ -255,6 +465,15 @@ __global__ void init_stats_kernel(unsigned long long* st, uint64_t hist_lo, uint
     else if (i == LC_ST_HIST_BINS) v = hist_bins;
     st[i] = v;
   }
+  if (queues)
+    for (uint64_t q = i0; q < nq; q += stride) queues[q * kQueueStride] = 0ull;
+  if (exhausted && i0 == 0) *exhausted = 0u;
+}
+
+__global__ void smid_probe_kernel(unsigned int* flags) {
+  uint32_t smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  if (threadIdx.x == 0) flags[smid & 1023u] = 1u;
 }
 
 template <class S, bool SF>
@@ -275,11 +494,17 @@ int occupancy_t() {
 }  // namespace
 
 cudaError_t launch_init_stats(uint64_t* stats, uint64_t hist_lo, uint32_t hist_shift, uint32_t hist_bins,
+                              unsigned long long* queues, uint32_t nq, unsigned int* exhausted,
                               cudaStream_t stream) {
-  const uint64_t words = LC_ST_HEADER + hist_bins + 2ull;
+  const uint64_t words = std::max<uint64_t>(LC_ST_HEADER + hist_bins + 2ull, nq);
   const unsigned g = static_cast<unsigned>(std::min<uint64_t>((words + 255) / 256, 1024));
   init_stats_kernel<<<g, 256, 0, stream>>>(reinterpret_cast<unsigned long long*>(stats), hist_lo, hist_shift,
-                                           hist_bins);
+                                           hist_bins, queues, nq, exhausted);
+  return cudaGetLastError();
+}
+
+cudaError_t probe_smids(int sms, unsigned int* d_flags, cudaStream_t stream) {
+  smid_probe_kernel<<<sms * 16, 32, 0, stream>>>(d_flags);
   return cudaGetLastError();
 }
 
