@@ -142,6 +142,10 @@ def main() -> None:
     ap.add_argument("--batch-log2", type=int, default=22)
     ap.add_argument("--workload-log2", type=int, default=24)
     ap.add_argument("--refill", type=int, default=0)
+    ap.add_argument("--starts", default="k0", choices=["k0", "random"],
+                    help="k0: special nodes (the metric's workload); random: uniform valid states")
+    ap.add_argument("--legs", type=int, default=1)
+    ap.add_argument("--stride", type=int, default=STRIDE)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -181,15 +185,22 @@ def main() -> None:
     hist_lo, hist_shift, hist_bins = 11_184_809 - (1 << 15), 0, 1 << 16
     words = N.ST_HEADER + hist_bins + 2
 
-    # this rank's contiguous shard of one global K0 stream, resident in HBM
-    allstarts = torch.empty((rank + 1) * per_gpu, dtype=torch.int64, device=dev)
-    N.check(N.lib.lc_random_candidates_device(ctx.handle, C.byref(sspec), params.fixed_r3, SEED,
-                                              allstarts.numel(), C.c_void_p(allstarts.data_ptr()),
-                                              C.c_void_p(stream.cuda_stream)))
-    starts = allstarts[rank * per_gpu:].clone()
-    del allstarts
-    dst = torch.empty(batch, dtype=torch.int64, device=dev)
-    dist_ = torch.empty(batch, dtype=torch.int64, device=dev)
+    if args.starts == "k0":
+        # this rank's contiguous shard of one global K0 stream, resident in HBM
+        allstarts = torch.empty((rank + 1) * per_gpu, dtype=torch.int64, device=dev)
+        N.check(N.lib.lc_random_candidates_device(ctx.handle, C.byref(sspec), params.fixed_r3, SEED,
+                                                  allstarts.numel(), C.c_void_p(allstarts.data_ptr()),
+                                                  C.c_void_p(stream.cuda_stream)))
+        starts = allstarts[rank * per_gpu:].clone()
+        del allstarts
+    else:
+        rng = np.random.default_rng(SEED + rank)
+        regs = [rng.integers(1, m + 1, size=per_gpu, dtype=np.uint64) for m in spec.reg_masks]
+        host = regs[0] | (regs[1] << np.uint64(19)) | (regs[2] << np.uint64(41))
+        starts = torch.from_numpy(host.view(np.int64)).to(dev)
+    STRIDE_, LEGS = args.stride, args.legs
+    dst = torch.empty(batch * LEGS, dtype=torch.int64, device=dev)
+    dist_ = torch.empty(batch * LEGS, dtype=torch.int64, device=dev)
     stats = torch.zeros((max(args.steps, 1), words), dtype=torch.int64, device=dev)
     wstats = torch.zeros(words, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -197,7 +208,7 @@ def main() -> None:
     def walk(b: int, out_stats) -> None:
         s = starts[b * batch:(b + 1) * batch]
         N.check(N.lib.lc_walk_device(ctx.handle, C.byref(sspec), params.fixed_r3, C.c_void_p(s.data_ptr()),
-                                     s.numel(), STRIDE, CAP, 1,
+                                     s.numel(), STRIDE_, CAP, LEGS,
                                      args.refill, C.c_void_p(dst.data_ptr()), C.c_void_p(dist_.data_ptr()),
                                      hist_lo, hist_shift, hist_bins, C.c_void_p(out_stats.data_ptr()),
                                      C.c_void_p(stream.cuda_stream)))
@@ -308,9 +319,10 @@ def main() -> None:
             "vs_baseline": value / PAPER_GTX580,
             "vs_baseline_ref": "paper GTX 580 bitsliced walk, 9,800 nodes/s x 11.17e6 clocks (PAPER.md:478-479)",
             "dtype": "u32 (bitsliced words, 32 lanes)", "data": "synthetic (K0 seeded special A5/1 nodes)",
-            "config": {"workload": f"configs[1]: 2^{args.workload_log2} special A5/1 start nodes per GPU, "
-                                   f"walked to the next special node, stride {STRIDE}; one step = one batch of "
-                                   f"2^{args.batch_log2}", "starts_per_step_per_gpu": batch,
+            "config": {"workload": f"configs[1]: 2^{args.workload_log2} "
+                                   f"{'special A5/1 start nodes' if args.starts == 'k0' else 'uniform random A5/1 states'}"
+                                   f" per GPU, walked {LEGS} hop(s) to the next special node, stride {STRIDE_}; "
+                                   f"one step = one batch of 2^{args.batch_log2}", "starts_per_step_per_gpu": batch,
                        "parallelism": f"dp{world} (independent start shards, stats all-reduce only)",
                        "l2": "flushed (256 MiB write) before every step", "refill": args.refill or "auto"},
             "gpu_launches": launches,

@@ -1,0 +1,135 @@
+"""Steps 1-2 feeding the walk (BASELINE.json configs[2]): special-node enumeration with
+the leaf/predecessor filter over a 2^32-state slice of the fixed-R3 plane (K2), the
+step-2 prune of the resulting candidates (K3), and a walk of the survivors (K1).
+
+    python bench_steps12.py [--rows-log2 13] [--prune-log2 20] [--depth 3000]
+
+Prints one JSON line.  Parity: the first 4 R2 rows of the slice and a 2048-candidate
+sample of the prune are compared with the C oracle on the host.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+R2_0 = 0x2AAA  # first R2 row of the slice
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rows-log2", type=int, default=13)   # 2^13 rows x (2^19-1) = 2^32 states
+    ap.add_argument("--prune-log2", type=int, default=20)
+    ap.add_argument("--depth", type=int, default=3000)     # the paper's DFS depth
+    ap.add_argument("--walk-log2", type=int, default=14)
+    args = ap.parse_args()
+
+    import torch
+
+    import paper_1210_6411_b200 as lc
+    from oracle import port
+    from paper_1210_6411_b200 import _native as N
+
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    spec = lc.A51
+    params = lc.CandidateParams.from_spec(spec, 0x2AAA00)
+    ctx = N.context(0)
+    sspec = N.spec_struct(spec)
+    rows = 1 << args.rows_log2
+    states = rows * spec.reg_masks[0]
+    cap = states // 2 + (1 << 20)
+
+    out = torch.empty(cap, dtype=torch.int64, device=dev)
+    count = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def enumerate_slice():
+        N.check(N.lib.lc_enumerate_device(ctx.handle, C.byref(sspec), params.fixed_r3, R2_0, R2_0 + rows,
+                                          C.c_void_p(out.data_ptr()), cap, C.c_void_p(count.data_ptr()),
+                                          C.c_void_p(stream.cuda_stream)))
+
+    enumerate_slice()  # warm-up
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 3
+    e0.record(stream)
+    for _ in range(reps):
+        enumerate_slice()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    k2_s = e0.elapsed_time(e1) / 1e3 / reps
+    ncand = int(count.item())
+
+    # parity: first 4 rows vs the C oracle (host)
+    want = port.enumerate_rows(spec, 0x2AAA00, R2_0, R2_0 + 4)
+    got = out[: want.size].cpu().numpy().view(np.uint64)
+    k2_parity = bool((got == want).all())
+    # size-independent checks over the whole slice: ascending, all on the fixed plane
+    head = out[:ncand]
+    ascending = bool((head[1:] > head[:-1]).all().item()) if ncand > 1 else True
+
+    # ---- K3: prune a prefix of the enumerated candidates (DFS, depth limit)
+    npr = min(1 << args.prune_log2, ncand)
+    cands = out[:npr].clone()
+    removed = torch.empty(npr, dtype=torch.uint8, device=dev)
+    work = torch.empty(npr, dtype=torch.int64, device=dev)
+
+    def prune():
+        N.check(N.lib.lc_prune_device(ctx.handle, C.byref(sspec), params.fixed_r3, 0, args.depth,
+                                      C.c_void_p(cands.data_ptr()), npr, C.c_void_p(removed.data_ptr()),
+                                      C.c_void_p(work.data_ptr()), C.c_void_p(stream.cuda_stream)))
+
+    prune()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    prune()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    k3_s = e0.elapsed_time(e1) / 1e3
+    expanded = int(work.sum().item())
+    nremoved = int(removed.sum().item())
+    # parity on a sample (oracle on host cores)
+    idx = np.linspace(0, npr - 1, min(2048, npr)).astype(np.int64)
+    sample = cands.cpu().numpy().view(np.uint64)[idx]
+    t0 = time.perf_counter()
+    o_removed, o_work = port.prune(spec, 0x2AAA00, "dfs", args.depth, sample)
+    cpu_s = time.perf_counter() - t0
+    k3_parity = bool((o_removed == removed.cpu().numpy()[idx]).all() and
+                     (o_work == work.cpu().numpy().view(np.uint64)[idx]).all())
+
+    # ---- K1: walk (a prefix of) the survivors to their next special node
+    surv = cands[removed == 0]
+    nw = min(1 << args.walk_log2, surv.numel())
+    res = lc.walk_arrays(surv[:nw].cpu().numpy().view(np.uint64), params, spec, stride=lc.DEFAULT_STRIDE_A51)
+
+    line = {
+        "metric": "steps 1-2 feeding the walk (special-node enumeration + leaf/predecessor filter, prune)",
+        "config": {"workload": f"configs[2]: R3 = 0x2AAA00, R2 in [{R2_0:#x}, {R2_0 + rows:#x}), all R1 "
+                               f"({states} states)", "prune": f"dfs depth {args.depth} on the first {npr} candidates"},
+        "k2_enumerate": {"states": states, "candidates": ncand, "seconds": k2_s, "states_per_s": states / k2_s,
+                         "candidates_per_s": ncand / k2_s, "bytes_written_per_s": ncand * 8 / k2_s,
+                         "hbm_frac_of_copy_peak": ncand * 8 / k2_s / 6546.2e9,
+                         "parity_first_4_rows_vs_oracle": k2_parity, "ascending": ascending},
+        "k3_prune": {"candidates": npr, "removed": nremoved, "removed_fraction": nremoved / npr,
+                     "expanded": expanded, "seconds": k3_s, "candidates_per_s": npr / k3_s,
+                     "expansions_per_s": expanded / k3_s, "parity_sample_vs_oracle": k3_parity,
+                     "cpu_port_expansions_per_s": float(o_work.sum()) / cpu_s,
+                     "cpu_port_cores": len(os.sched_getaffinity(0))},
+        "k1_walk_survivors": {"walks": nw, "edges": res.edges, "transitions": res.transitions},
+        "gpu": torch.cuda.get_device_name(0),
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -140,6 +140,9 @@ int lc_enumerate_device(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3, uin
  * per-candidate `expanded` counter (LIFO order replicated). */
 int lc_prune(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3, int32_t mode, uint64_t limit,
              const uint64_t *cands, uint64_t n, uint8_t *removed, uint64_t *work);
+int lc_prune_device(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3, int32_t mode,
+                    uint64_t limit, const uint64_t *d_cands, uint64_t n, uint8_t *d_removed,
+                    uint64_t *d_work, void *stream);
 
 /* Seeded synthetic start set (K0): the first n special nodes of the
  * counter-based stream trial i -> (r1, r2) = split(splitmix64(seed + i*golden)), in trial

@@ -70,6 +70,8 @@ _SIGNATURES = {
                              _vp, _vp], C.c_int),
     "lc_prune": ([_vp, C.POINTER(lc_spec), C.c_uint64, C.c_int32, C.c_uint64, _u64p, C.c_uint64, _u8p,
                   _u64p], C.c_int),
+    "lc_prune_device": ([_vp, C.POINTER(lc_spec), C.c_uint64, C.c_int32, C.c_uint64, _vp, C.c_uint64, _vp, _vp,
+                         _vp], C.c_int),
     "lc_random_candidates": ([_vp, C.POINTER(lc_spec), C.c_uint64, C.c_uint64, C.c_uint64, _u64p, _u64p],
                              C.c_int),
     "lc_random_candidates_device": ([_vp, C.POINTER(lc_spec), C.c_uint64, C.c_uint64, C.c_uint64, _vp, _vp],

@@ -115,7 +115,7 @@ struct lc_ctx {
   int device = 0;
   int sms = 0;
   cudaStream_t stream = nullptr;
-  DevBuf meta, queue, stats, a, b, c, d, scratch, smmap;
+  DevBuf meta, queue, stats, a, b, c, d, scratch, smmap, pq;
   int mapped_sms = -1;  // SMs found by the %smid probe (-1: not probed yet)
 };
 
@@ -181,7 +181,7 @@ int lc_ctx_destroy(lc_ctx* ctx) {
   if (!ctx) return LC_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  for (DevBuf* b : {&ctx->meta, &ctx->queue, &ctx->stats, &ctx->a, &ctx->b, &ctx->c, &ctx->d, &ctx->scratch, &ctx->smmap})
+  for (DevBuf* b : {&ctx->meta, &ctx->queue, &ctx->stats, &ctx->a, &ctx->b, &ctx->c, &ctx->d, &ctx->scratch, &ctx->smmap, &ctx->pq})
     b->release();
   cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -398,7 +398,7 @@ int lc_enumerate_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, uin
   if (r2_lo < 1 || r2_hi > (1ull << l2) || r2_lo > r2_hi)
     return fail(LC_ERR_ARG, "R2 rows must satisfy 1 <= r2_lo <= r2_hi <= 2^%d", l2);
   LC_CUDA(cudaSetDevice(ctx->device));
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
   const uint64_t words = lc::enumerate_scratch_words(id, r2_lo, r2_hi);
   LC_CUDA(ctx->scratch.ensure(words * 8));
   int launches = 0;
@@ -445,7 +445,7 @@ int lc_random_candidates_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed
   if ((rc = check_fixed(id, fixed_r3))) return rc;
   if (n == 0) return LC_OK;
   LC_CUDA(cudaSetDevice(ctx->device));
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
   uint64_t trials = static_cast<uint64_t>(static_cast<double>(n) / acceptance_estimate(id)) + 65536;
   for (int attempt = 0; attempt < 8; ++attempt) {
     const uint64_t words = lc::random_scratch_words(trials);
@@ -484,8 +484,8 @@ int lc_random_candidates(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, ui
 
 // ------------------------------------------------------------------------ prune (K3)
 
-int lc_prune(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int32_t mode, uint64_t limit,
-             const uint64_t* cands, uint64_t n, uint8_t* removed, uint64_t* work) {
+int lc_prune_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int32_t mode, uint64_t limit,
+                    const uint64_t* d_cands, uint64_t n, uint8_t* d_removed, uint64_t* d_work, void* stream) {
   if (!ctx) return fail(LC_ERR_ARG, "null context");
   lc::SpecId id;
   int rc = check_spec(spec, &id);
@@ -495,17 +495,28 @@ int lc_prune(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int32_t mode, 
   if (limit < 1) return fail(LC_ERR_ARG, "limit must be >= 1");
   if (n == 0) return LC_OK;
   LC_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  LC_CUDA(ctx->pq.ensure(8));
+  LC_CUDA(cudaMemsetAsync(ctx->pq.p, 0, 8, st));
+  const int blocks = lc::prune_blocks_per_sm(id) * ctx->sms;
+  LC_CUDA(lc::launch_prune(id, static_cast<uint32_t>(fixed_r3), mode, limit, d_cands, n, d_removed, d_work,
+                           ctx->pq.as<unsigned long long>(), blocks, st));
+  g_launches += 1;
+  return LC_OK;
+}
+
+int lc_prune(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int32_t mode, uint64_t limit,
+             const uint64_t* cands, uint64_t n, uint8_t* removed, uint64_t* work) {
+  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  if (n == 0) return LC_OK;
+  LC_CUDA(cudaSetDevice(ctx->device));
   LC_CUDA(ctx->a.ensure(n * 8));
   LC_CUDA(ctx->b.ensure(n));
   LC_CUDA(ctx->c.ensure(n * 8));
-  LC_CUDA(ctx->queue.ensure(8));
   LC_CUDA(cudaMemcpyAsync(ctx->a.p, cands, n * 8, cudaMemcpyHostToDevice, ctx->stream));
-  LC_CUDA(cudaMemsetAsync(ctx->queue.p, 0, 8, ctx->stream));
-  const int blocks = lc::prune_blocks_per_sm(id) * ctx->sms;
-  LC_CUDA(lc::launch_prune(id, static_cast<uint32_t>(fixed_r3), mode, limit, ctx->a.as<uint64_t>(), n,
-                           ctx->b.as<uint8_t>(), ctx->c.as<uint64_t>(), ctx->queue.as<unsigned long long>(),
-                           blocks, ctx->stream));
-  g_launches += 1;
+  int rc = lc_prune_device(ctx, spec, fixed_r3, mode, limit, ctx->a.as<uint64_t>(), n, ctx->b.as<uint8_t>(),
+                           ctx->c.as<uint64_t>(), ctx->stream);
+  if (rc) return rc;
   LC_CUDA(cudaMemcpyAsync(removed, ctx->b.p, n, cudaMemcpyDeviceToHost, ctx->stream));
   LC_CUDA(cudaMemcpyAsync(work, ctx->c.p, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
   LC_CUDA(cudaStreamSynchronize(ctx->stream));
