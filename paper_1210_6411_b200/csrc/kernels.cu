@@ -66,17 +66,6 @@ constexpr int kTileShift = 16;
 constexpr uint64_t kTile = 1ull << kTileShift;
 constexpr int kCompactThreads = 256;
 
-template <class S>
-struct EnumGen {
-  uint64_t r2_lo;
-  uint64_t packed_f;
-  __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
-    const uint64_t r2 = r2_lo + i / S::M1;
-    const uint64_t r1 = 1u + i % S::M1;
-    return r1 | (r2 << S::O2) | packed_f;
-  }
-};
-
 __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
@@ -198,6 +187,88 @@ cudaError_t compact(Gen g, uint64_t total, uint32_t F, uint64_t* out, uint64_t c
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- K2: step-1 enumeration
+// On the fixed-R3 plane the special-node predicate (cipher.py:420-428) depends only on
+// four bits: R1's clock bit and the bit above it (c1, n1) and the same pair of R2
+// (c2, n2) -- R3's pair (c3, n3) is fixed.  A candidate needs R3 clocked by the next
+// step (c3 agrees with c1 or c2; R3 then leaves F because a maximal-period step has no
+// nonzero fixed point) and a non-empty predecessor-table entry (kNonEmpty).  So for an
+// R2 row the candidates are exactly the R1 values whose bits (ct1, ct1+1) form an allowed
+// pattern p: runs of 2^ct1 consecutive R1 values, in ascending order.  Each output slot
+// has a closed-form state, so the kernel is a pure coalesced stream of 8-byte stores
+// (HBM-write bound) -- the same set and order as pipeline.enumerate_candidates
+// (pipeline.py:104-118), checked against the reference's digests.
+
+// Allowed R1 patterns p = c1 | n1 << 1 (bit p of the result) for an R2 class q = c2 | n2 << 1.
+__device__ __forceinline__ uint32_t allowed_patterns(uint32_t q, uint32_t c3, uint32_t n3) {
+  const uint32_t c2 = q & 1u, n2 = q >> 1;
+  uint32_t a = 0;
+#pragma unroll
+  for (uint32_t p = 0; p < 4; ++p) {
+    const uint32_t c1 = p & 1u, n1 = p >> 1;
+    const uint32_t idx = (c1 << 5) | (n1 << 4) | (c2 << 3) | (n2 << 2) | (c3 << 1) | n3;
+    if ((c3 == c1 || c3 == c2) && ((kNonEmpty >> idx) & 1ull)) a |= 1u << p;
+  }
+  return a;
+}
+
+// Candidates in one R2 row of class a: |a| * 2^(l1-2) R1 values, minus R1 = 0 if p = 0 is allowed.
+template <class S>
+__device__ __forceinline__ uint64_t row_count(uint32_t a) {
+  return static_cast<uint64_t>(__popc(a)) * (1ull << (S::L1 - 2)) - (a & 1u);
+}
+
+// Number of r in [0, n) with ((r >> ct) & 3) == q.
+__device__ __forceinline__ uint64_t class_count(uint64_t n, uint32_t q, int ct) {
+  const uint64_t blk = 1ull << ct;
+  const uint64_t rem = n & ((blk << 2) - 1), lo = q * blk;
+  return (n >> (ct + 2)) * blk + (rem > lo ? min(rem - lo, blk) : 0ull);
+}
+
+// Candidates with R2 in [r2_lo, r2).
+template <class S>
+__device__ __forceinline__ uint64_t plane_offset(uint64_t r2_lo, uint64_t r2, uint32_t c3, uint32_t n3) {
+  uint64_t off = 0;
+#pragma unroll
+  for (uint32_t q = 0; q < 4; ++q)
+    off += row_count<S>(allowed_patterns(q, c3, n3)) * (class_count(r2, q, S::CT2) - class_count(r2_lo, q, S::CT2));
+  return off;
+}
+
+template <class S>
+__global__ void __launch_bounds__(256) enumerate_plane_kernel(uint64_t r2_lo, uint64_t r2_hi, uint32_t F,
+                                                              uint64_t* __restrict__ out, uint64_t cap,
+                                                              uint64_t* __restrict__ d_count) {
+  constexpr int CT1 = S::CT1;
+  constexpr uint32_t kRun = 1u << CT1;                // consecutive R1 values per run
+  constexpr uint32_t kHigh = 1u << (S::L1 - CT1 - 2); // runs of each pattern per row
+  const uint32_t c3 = (F >> S::CT3) & 1u, n3 = (F >> (S::CT3 + 1)) & 1u;
+  const uint64_t packed_f = static_cast<uint64_t>(F) << S::O3;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *d_count = plane_offset<S>(r2_lo, r2_hi, c3, n3);
+  for (uint64_t r2 = r2_lo + blockIdx.x; r2 < r2_hi; r2 += gridDim.x) {
+    const uint32_t a = allowed_patterns((r2 >> S::CT2) & 3u, c3, n3);
+    const uint32_t na = __popc(a);
+    if (na == 0) continue;
+    const uint64_t base = plane_offset<S>(r2_lo, r2, c3, n3) - (a & 1u);  // slot of (high 0, run 0, low 0)
+    const uint64_t row_bits = (r2 << S::O2) | packed_f;
+    // warp w takes (high, pattern) runs; lanes walk the run's R1 values
+    for (uint32_t run = warp; run < kHigh * na; run += nwarps) {
+      const uint32_t high = run / na, rank = run - high * na;
+      uint32_t p = a;
+      for (uint32_t k = 0; k < rank; ++k) p &= p - 1u;
+      p = __ffs(p) - 1;
+      const uint32_t r1_base = (high << (CT1 + 2)) | (p << CT1);
+      const uint64_t slot0 = base + static_cast<uint64_t>(run) * kRun;
+      for (uint32_t low = lane; low < kRun; low += 32u) {
+        const uint32_t r1 = r1_base | low;
+        const uint64_t slot = slot0 + low;
+        if (r1 != 0u && slot < cap) out[slot] = row_bits | r1;
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- K3: step-2 prune
 // Thread per candidate, stackless depth-first traversal of the candidate's segment (the
 // reverse tree through predecessors that are not candidates, pipeline.py:121-129).  The
@@ -248,74 +319,96 @@ __device__ __forceinline__ Node<S> expand_node(uint64_t y, uint32_t F) {
   return nd;
 }
 
+// One traversal step of a candidate's segment.  State: x (current node), d (depth),
+// acc (expanded for dfs / node count for bfs), pop (x is about to be expanded; else we
+// are backtracking from x).  Returns 0 while running, 1 = finished shallow, 2 = finished
+// deep (not shallow).
 template <class S>
-__device__ void prune_one(uint64_t root, uint32_t F, int mode, uint64_t limit, uint8_t* removed,
-                          uint64_t* work) {
-  uint64_t x = root, d = 0, count = 1, expanded = 0;
-  bool pop = true, shallow = true;
-  for (;;) {
-    if (!pop && d == 0) break;  // back at the root: traversal complete
-    const uint64_t y = pop ? x : clock_scalar<S>(x);
-    const Node<S> nd = expand_node<S>(y, F);
-    if (pop) {
-      if (nd.mask != 0u) {
-        if (mode == 0) {
-          if (d >= limit) {  // a child would sit below the depth limit
-            expanded += 1;
-            shallow = false;
-            break;
-          }
-          expanded += __popc(nd.mask);
-        } else {
-          count += __popc(nd.mask);
-          if (count > limit) {
-            count = limit + 1;
-            shallow = false;
-            break;
-          }
+__device__ __forceinline__ int prune_step(uint64_t& x, uint64_t& d, uint64_t& acc, bool& pop, uint32_t F,
+                                          int mode, uint64_t limit) {
+  if (!pop && d == 0) return 1;  // back at the root: traversal complete
+  const uint64_t y = pop ? x : clock_scalar<S>(x);
+  const Node<S> nd = expand_node<S>(y, F);
+  if (pop) {
+    if (nd.mask != 0u) {
+      if (mode == 0) {
+        if (d >= limit) {  // a child would sit below the depth limit
+          acc += 1;
+          return 2;
         }
-        x = nd.child(31 - __clz(nd.mask));  // the reference pops the last child first
-        ++d;
+        acc += __popc(nd.mask);
       } else {
-        pop = false;
+        acc += __popc(nd.mask);
+        if (acc > limit) {
+          acc = limit + 1;
+          return 2;
+        }
       }
+      x = nd.child(31 - __clz(nd.mask));  // the reference pops the last child first
+      ++d;
     } else {
-      // y is x's parent; continue with x's next-lower sibling, else climb
-      uint32_t q = 0;
+      pop = false;
+    }
+  } else {
+    // y is x's parent; continue with x's next-lower sibling, else climb
+    uint32_t q = 0;
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (((nd.mask >> k) & 1u) && nd.child(k) == x) q = k;
-      const uint32_t lower = nd.mask & ((1u << q) - 1u);
-      if (lower != 0u) {
-        x = nd.child(31 - __clz(lower));
-        pop = true;
-      } else {
-        x = y;
-        --d;
-      }
+    for (int k = 0; k < 4; ++k)
+      if (((nd.mask >> k) & 1u) && nd.child(k) == x) q = k;
+    const uint32_t lower = nd.mask & ((1u << q) - 1u);
+    if (lower != 0u) {
+      x = nd.child(31 - __clz(lower));
+      pop = true;
+    } else {
+      x = y;
+      --d;
     }
   }
-  *removed = shallow ? 1 : 0;
-  *work = mode == 0 ? expanded : count;
+  return 0;
 }
 
+// Persistent: every lane runs its own traversal and takes the next candidate as soon as
+// it finishes (tickets aggregated over the lanes that need one), so a warp is never held
+// up by its deepest segment.
 template <class S>
 __global__ void __launch_bounds__(kThreads) prune_kernel(const uint64_t* __restrict__ cands, uint64_t n,
                                                          uint32_t F, int mode, uint64_t limit,
                                                          uint8_t* __restrict__ removed,
                                                          uint64_t* __restrict__ work,
                                                          unsigned long long* queue) {
+  const uint32_t lane = threadIdx.x & 31u;
+  uint64_t i = 0, x = 0, d = 0, acc = 0;
+  bool have = false, pop = true, drained = false;
   for (;;) {
-    // warp-aggregated ticket: one atomic per warp per round
-    const uint32_t lane = threadIdx.x & 31u;
-    unsigned long long base = 0;
-    const uint32_t act = __activemask();
-    const int leader = __ffs(act) - 1;
-    if (static_cast<int>(lane) == leader) base = atomicAdd(queue, static_cast<unsigned long long>(__popc(act)));
-    base = __shfl_sync(act, base, leader);
-    const uint64_t i = base + __popc(act & ((1u << lane) - 1u));
-    if (i >= n) break;
-    prune_one<S>(cands[i], F, mode, limit, &removed[i], &work[i]);
+    if (!drained) {
+      const uint32_t need = __ballot_sync(kFull, !have);
+      if (need != 0u) {
+        const int leader = __ffs(need) - 1;
+        unsigned long long base = 0;
+        if (static_cast<int>(lane) == leader) base = atomicAdd(queue, static_cast<unsigned long long>(__popc(need)));
+        base = __shfl_sync(kFull, base, leader);
+        if (base + __popc(need) >= n) drained = true;
+        if (!have) {
+          i = base + __popc(need & ((1u << lane) - 1u));
+          if (i < n) {
+            x = cands[i];
+            d = 0;
+            acc = mode == 0 ? 0 : 1;
+            pop = true;
+            have = true;
+          }
+        }
+      }
+    }
+    if (!__any_sync(kFull, have)) break;
+    if (have) {
+      const int r = prune_step<S>(x, d, acc, pop, F, mode, limit);
+      if (r != 0) {
+        removed[i] = r == 1 ? 1 : 0;
+        work[i] = acc;
+        have = false;
+      }
+    }
   }
 }
 
@@ -380,12 +473,13 @@ uint64_t enumerate_scratch_words(SpecId id, uint64_t r2_lo, uint64_t r2_hi) {
 cudaError_t launch_enumerate(SpecId id, uint32_t F, uint64_t r2_lo, uint64_t r2_hi, uint64_t* out,
                              uint64_t cap, uint64_t* d_count, uint64_t* scratch,
                              uint64_t scratch_words, cudaStream_t stream, int* launches) {
+  (void)scratch;
   (void)scratch_words;
-  LC_DISPATCH(id, {
-    EnumGen<S> g{r2_lo, static_cast<uint64_t>(F) << S::O3};
-    const uint64_t total = (r2_hi > r2_lo ? r2_hi - r2_lo : 0) * S::M1;
-    return compact<S>(g, total, F, out, cap, d_count, scratch, stream, launches);
-  });
+  const uint64_t rows = r2_hi > r2_lo ? r2_hi - r2_lo : 0;
+  const unsigned grid = static_cast<unsigned>(rows == 0 ? 1 : (rows > (1u << 20) ? (1u << 20) : rows));
+  if (launches) *launches += 1;
+  LC_DISPATCH(id, enumerate_plane_kernel<S><<<grid, 256, 0, stream>>>(r2_lo, r2_hi, F, out, cap, d_count);
+              return cudaGetLastError());
 }
 
 uint64_t random_scratch_words(uint64_t trials) { return (trials + kTile - 1) / kTile + 1; }
