@@ -37,6 +37,10 @@ LOP3_PER_TRANSITION = 72 / 32      # algorithmic LOP3 per A5/1
 SEED = 1210_6411
 STRIDE = 11_170_000
 CAP = 178_957_008  # the reference's default walk cap for A5/1 (bitslice.py:273-274)
+PAPER_SCALE_TRANSITIONS = int(2 ** 33.6 * 11_184_857)  # ~1.46e17
+# DRAM bytes per walk of the walk kernel: dram__bytes_read.sum + dram__bytes_write.sum of
+# one ncu capture (profiles/r01_walk_a51_metrics.json, a 2^20-walk launch) / walks
+TRAFFIC_BYTES_PER_WALK = (9.219072e6 + 21.899008e6) / (1 << 20)
 
 
 def host_cores() -> int:
@@ -328,13 +332,22 @@ def main() -> None:
             "gpu_launches": launches,
             "walk_stats": {k: summ[k] for k in ("edges", "transitions", "mean", "sd", "min", "max") if k in summ},
             "roofline": {"bound": "int-alu (LOP3 issue)", "achieved": achieved / 1e12, "peak": lop3_peak / 1e12,
-                         "unit": "TLOP3/s", "frac": achieved / lop3_peak, "traffic": None,
+                         "unit": "TLOP3/s", "frac": achieved / lop3_peak,
+                         "traffic": TRAFFIC_BYTES_PER_WALK * batch,
+                         "traffic_note": "DRAM bytes per launch: ncu dram__bytes_read+write per walk "
+                                         "(profiles/r01_walk_a51_metrics.json) x walks per launch; "
+                                         "algorithmic 24 B/walk (8 in, 16 out)",
                          "algorithmic": "2.25 LOP3 per transition (72 per 32-lane step)",
                          "kernel_ms_per_launch": 1e3 * sum(kernel_s) / len(kernel_s),
                          "peak_source": f"measured lop3 microbenchmark ({peak_mhz:.0f} MHz), "
                                         f"spec {sms}x64x{(clk.get('sm_max_mhz') or 1965):.0f} MHz = "
                                         f"{sms * 64 * (clk.get('sm_max_mhz') or 1965) * 1e6 / 1e12:.2f} T/s"},
             "clocks": clk,
+            # configs[4]: paper-scale step 3 (~2^33.6 skeleton nodes x 11,184,857 clocks,
+            # PAPER.md:490, :672) at this run's per-GPU rate on 8 GPUs
+            "projection": {"paper_scale_transitions": PAPER_SCALE_TRANSITIONS,
+                           "hours_on_8_gpus": PAPER_SCALE_TRANSITIONS / (8 * value / world) / 3600,
+                           "paper": "9 d 3 h on 5x Tesla C1060; 4 d 8 h projected on 5x GTX 580 (PAPER.md:486-487)"},
             "e2e": e2e,
             "cpu_baseline": cpu,
         }

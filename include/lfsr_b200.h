@@ -36,6 +36,9 @@ extern "C" {
 #define LC_ERR_INVALID_STATE (-5)/* a start has a zero register; the reference
                                     walks it to the cap and raises StrideError */
 #define LC_ERR_OVERFLOW (-6)     /* output capacity too small */
+#define LC_ERR_UNSORTED (-7)     /* edge records not sorted by unique source (records.py:3-5) */
+#define LC_ERR_NOT_CLOSED (-8)   /* a removed leaf's destination has no record (reduce.py:182-184) */
+#define LC_ERR_NOT_PERMUTATION (-9) /* count_cycles input is not a permutation (reduce.py:226-246) */
 
 /* Cipher instance (cipher.py:57-170 CipherSpec): register lengths, feedback tap masks
  * (bit i set = tap at register bit i) and clock tap positions. */
@@ -156,6 +159,31 @@ int lc_random_candidates_device(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed
  * queries[i] not in the ascending array `sorted_set`, or n if all are members. */
 int lc_first_missing(lc_ctx *ctx, const uint64_t *sorted_set, uint64_t m, const uint64_t *queries,
                      uint64_t n, uint64_t *first_missing);
+
+/* ------------------------------------------- steps 4-5: edge output, leaf cutting, cycles */
+
+/* Edge-output stage: sort skeleton edge records ascending by source, in place (host
+ * buffers; subtree_size / subtree_depth may be NULL).  Produces the order write_edges
+ * and step 4 require (records.py:3-5, reduce.py:3-4). */
+int lc_sort_edges(lc_ctx *ctx, uint64_t n, uint64_t *src, uint64_t *dst, uint64_t *dist,
+                  uint64_t *subtree_size, uint64_t *subtree_depth);
+
+/* Replaces reduce.cut_leaves_pass (reduce.py:118-186; max_passes = 1) and
+ * cut_leaves_to_fixpoint (reduce.py:189-223; max_passes = 0) on records held in host
+ * buffers (SoA, sorted by unique source), in place: the first *n_out records are the
+ * survivors in source order with folded subtree sizes/depths.  pass_stats receives
+ * (leaves_removed, inner_nodes, out_size_sum) per pass, up to max_stats passes. */
+int lc_cut_leaves(lc_ctx *ctx, uint64_t n, uint64_t *src, uint64_t *dst, uint64_t *dist,
+                  uint64_t *subtree_size, uint64_t *subtree_depth, uint32_t max_passes,
+                  uint64_t *pass_stats, uint32_t max_stats, uint32_t *n_passes, uint64_t *n_out);
+
+/* Replaces reduce.count_cycles (reduce.py:226-266): cycles of a permutation, sorted by
+ * leader (smallest source on the cycle): hop count, clock length (sum of distances),
+ * aggregate tree size (sum of subtree sizes).  Output arrays hold up to n entries. */
+int lc_count_cycles(lc_ctx *ctx, uint64_t n, const uint64_t *src, const uint64_t *dst,
+                    const uint64_t *dist, const uint64_t *subtree_size, uint64_t *leader,
+                    uint64_t *hop_count, uint64_t *clock_length, uint64_t *tree_size,
+                    uint64_t *n_cycles);
 
 #ifdef __cplusplus
 }

@@ -11,6 +11,7 @@ Usage (from the repo root, in the build container):
     python oracle/gen_golden.py prune      # ~1 min: step-2 prune fixtures
     python oracle/gen_golden.py enumerate  # ~30 s: A5/1 step-1 sub-slice digest
     python oracle/gen_golden.py kat        # ~2 min: A5/1 seed-0 256-walk known answer
+    python oracle/gen_golden.py reduce     # ~1 min: steps 4-5 (leaf cutting, cycles) on minis
     python oracle/gen_golden.py c1 [W]     # ~1 h on 8 cores: the full 2^16 config-1 set
 
 Digest format: sha256 over lines
@@ -291,6 +292,64 @@ def gen_enumerate(ref):
     save_json("enumerate.json", out)
 
 
+def gen_reduce(ref):
+    """Steps 4-5 on mini skeletons (reduce.py:118-266): full candidate sets and pruned
+    skeletons, through the reference's own file-based pipeline."""
+    import tempfile
+
+    C, P, R, Rec = ref.cipher, ref.pipeline, ref.reduce, ref.records
+    table = C.build_predecessor_table()
+    out = {}
+    for spec in (C.MINI567, C.MINI789):
+        params = C.CandidateParams.from_spec(spec, C.default_fixed_r3(spec))
+        cands = mini_candidates(ref, spec, params, table)
+        gt = ref.oracle.brute_force_analysis(spec, params)
+        out[f"{spec.name}_oracle_cycles"] = [list(c) for c in gt.cycle_multiset()]
+        for label, cfg in (("full", None), ("dfs4", P.PruneConfig(mode="dfs", depth_limit=4)),
+                           ("bfs8", P.PruneConfig(mode="bfs", node_limit=8))):
+            skel = cands if cfg is None else P.prune_shallow_segments(cands, cfg, spec, params, table)[0]
+            edges = P.build_skeleton_edges(skel, params, spec, table)
+            with tempfile.TemporaryDirectory() as d:
+                src = os.path.join(d, "edges.bin")
+                dst = os.path.join(d, "fix.bin")
+                Rec.write_edges(src, edges)
+                one = os.path.join(d, "one.bin")
+                st1 = R.cut_leaves_pass(src, one, R.ReduceConfig())
+                one_recs = list(Rec.read_edges(one))
+                # cut_leaves_to_fixpoint (reduce.py:189-223) raises "subtree size conservation
+                # violated" on every input whose first pass removes a leaf: its expected total
+                # (reduce.py:210-212) counts pass-1 leaves twice.  Iterate the reference's
+                # own cut_leaves_pass to the fixpoint instead (what :203-219 intends).
+                passes, cur, gen = [], src, 0
+                while True:
+                    nxt = os.path.join(d, f"gen{gen}.bin")
+                    st = R.cut_leaves_pass(cur, nxt, R.ReduceConfig())
+                    passes.append(st)
+                    cur, gen = nxt, gen + 1
+                    if st.leaves_removed == 0:
+                        break
+                try:
+                    R.cut_leaves_to_fixpoint(src, dst, R.ReduceConfig())
+                    fixpoint_raises = None
+                except AssertionError as exc:
+                    fixpoint_raises = str(exc)
+                log = R.IterationLog(passes=passes)
+                fix = list(Rec.read_edges(cur))
+                cycles = R.count_cycles(cur)
+            out[f"{spec.name}_{label}"] = {
+                "skeleton": len(skel),
+                "pass1": {"leaves_removed": st1.leaves_removed, "inner_nodes": st1.inner_nodes,
+                          "out_size_sum": st1.out_size_sum, "records_digest": u64_digest(
+                              [v for r in one_recs for v in r])},
+                "passes": [[p.leaves_removed, p.inner_nodes, p.out_size_sum] for p in log.passes],
+                "iterations": log.iterations, "reference_fixpoint_raises": fixpoint_raises,
+                "fixpoint": [list(r) for r in fix],
+                "cycles": [list(c) for c in cycles],
+            }
+            print(spec.name, label, len(skel), "passes", len(log.passes), "cycles", len(cycles))
+    save_json("reduce.json", out)
+
+
 def c1_starts(ref, n):
     C, P = ref.cipher, ref.pipeline
     table = C.build_predecessor_table()
@@ -374,6 +433,8 @@ def main():
         gen_enumerate(ref)
     elif what == "kat":
         gen_kat(ref)
+    elif what == "reduce":
+        gen_reduce(ref)
     elif what == "c1":
         gen_c1(ref, int(sys.argv[2]) if len(sys.argv) > 2 else os.cpu_count())
     else:

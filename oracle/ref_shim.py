@@ -36,6 +36,6 @@ def load():
     import importlib
 
     ns = types.SimpleNamespace()
-    for name in ("cipher", "bitslice", "pipeline", "records", "oracle"):
+    for name in ("cipher", "bitslice", "pipeline", "records", "oracle", "extsort", "reduce"):
         setattr(ns, name, importlib.import_module(f"lfsrcycles.{name}"))
     return ns

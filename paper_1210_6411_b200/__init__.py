@@ -22,5 +22,8 @@ from .pipeline import (PruneConfig, PruneSoundnessError, PruneStats, auto_depth_
                        random_candidates_gpu)
 from .records import (EDGE_SIZE, ByteCounter, EdgeRecord, read_edge_arrays, read_edges,  # noqa: F401
                       read_states, write_edge_arrays, write_edges, write_states)
+from .reduce import (CycleRecord, IterationLog, NotAPermutationError, PassStats,  # noqa: F401
+                     ReduceConfig, count_cycles, count_cycles_arrays, cut_leaves_arrays,
+                     cut_leaves_pass, cut_leaves_to_fixpoint, sort_edge_arrays)
 
 __version__ = "0.1.0"

@@ -22,6 +22,9 @@ LC_ERR_UNSUPPORTED = -3
 LC_ERR_CAP = -4
 LC_ERR_INVALID_STATE = -5
 LC_ERR_OVERFLOW = -6
+LC_ERR_UNSORTED = -7
+LC_ERR_NOT_CLOSED = -8
+LC_ERR_NOT_PERMUTATION = -9
 
 # LC_ST_* (include/lfsr_b200.h)
 ST_EDGES, ST_TRANSITIONS, ST_MIN, ST_MAX, ST_SQ_LO, ST_SQ_HI = 0, 1, 2, 3, 4, 5
@@ -77,6 +80,11 @@ _SIGNATURES = {
     "lc_random_candidates_device": ([_vp, C.POINTER(lc_spec), C.c_uint64, C.c_uint64, C.c_uint64, _vp, _vp],
                                     C.c_int),
     "lc_first_missing": ([_vp, _u64p, C.c_uint64, _u64p, C.c_uint64, _u64p], C.c_int),
+    "lc_sort_edges": ([_vp, C.c_uint64, _u64p, _u64p, _u64p, _u64p, _u64p], C.c_int),
+    "lc_cut_leaves": ([_vp, C.c_uint64, _u64p, _u64p, _u64p, _u64p, _u64p, C.c_uint32, _u64p, C.c_uint32,
+                       C.POINTER(C.c_uint32), _u64p], C.c_int),
+    "lc_count_cycles": ([_vp, C.c_uint64, _u64p, _u64p, _u64p, _u64p, _u64p, _u64p, _u64p, _u64p, _u64p],
+                        C.c_int),
 }
 
 EXPORTED = tuple(_SIGNATURES)

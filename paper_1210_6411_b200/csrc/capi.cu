@@ -545,4 +545,105 @@ int lc_first_missing(lc_ctx* ctx, const uint64_t* sorted_set, uint64_t m, const 
   return LC_OK;
 }
 
+// ------------------------------------------------- steps 4-5: sort, leaf cutting, cycles
+
+static int reduce_error(unsigned int err) {
+  switch (err) {
+    case 1: return fail(LC_ERR_UNSORTED, "edge records are not sorted by unique source");
+    case 2: return fail(LC_ERR_NOT_CLOSED, "a removed leaf's destination has no surviving record; input was not closed");
+    case 3: return fail(LC_ERR_NOT_PERMUTATION, "a destination is not a source");
+    case 4: return fail(LC_ERR_NOT_PERMUTATION, "destinations are not a permutation of sources");
+    default: return LC_OK;
+  }
+}
+
+int lc_sort_edges(lc_ctx* ctx, uint64_t n, uint64_t* src, uint64_t* dst, uint64_t* dist, uint64_t* subtree_size,
+                  uint64_t* subtree_depth) {
+  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  if (n < 2) return LC_OK;
+  if (!src || !dst || !dist) return fail(LC_ERR_ARG, "null buffer");
+  LC_CUDA(cudaSetDevice(ctx->device));
+  const size_t nb = n * 8;
+  uint64_t* host[5] = {src, dst, dist, subtree_size, subtree_depth};
+  DevBuf* bufs[5] = {&ctx->a, &ctx->b, &ctx->c, &ctx->d, &ctx->stats};
+  uint64_t* dev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  for (int k = 0; k < 5; ++k) {
+    if (!host[k]) continue;
+    LC_CUDA(bufs[k]->ensure(nb));
+    dev[k] = bufs[k]->as<uint64_t>();
+    LC_CUDA(cudaMemcpyAsync(dev[k], host[k], nb, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  LC_CUDA(ctx->scratch.ensure(lc::sort_scratch_bytes(n)));
+  int launches = 0;
+  LC_CUDA(lc::sort_records_device(n, dev, 5, ctx->scratch.p, ctx->scratch.bytes, ctx->stream, &launches));
+  g_launches += launches;
+  for (int k = 0; k < 5; ++k)
+    if (host[k]) LC_CUDA(cudaMemcpyAsync(host[k], dev[k], nb, cudaMemcpyDeviceToHost, ctx->stream));
+  LC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LC_OK;
+}
+
+int lc_cut_leaves(lc_ctx* ctx, uint64_t n, uint64_t* src, uint64_t* dst, uint64_t* dist, uint64_t* subtree_size,
+                  uint64_t* subtree_depth, uint32_t max_passes, uint64_t* pass_stats, uint32_t max_stats,
+                  uint32_t* n_passes, uint64_t* n_out) {
+  if (!ctx || !n_passes || !n_out) return fail(LC_ERR_ARG, "null argument");
+  *n_passes = 0;
+  *n_out = n;
+  if (n == 0) return LC_OK;
+  if (!src || !dst || !dist || !subtree_size || !subtree_depth) return fail(LC_ERR_ARG, "null buffer");
+  LC_CUDA(cudaSetDevice(ctx->device));
+  const size_t nb = n * 8;
+  DevBuf* cols[5] = {&ctx->a, &ctx->b, &ctx->c, &ctx->d, &ctx->stats};
+  uint64_t* host[5] = {src, dst, dist, subtree_size, subtree_depth};
+  for (int k = 0; k < 5; ++k) {
+    LC_CUDA(cols[k]->ensure(nb));
+    LC_CUDA(cudaMemcpyAsync(cols[k]->p, host[k], nb, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  LC_CUDA(ctx->scratch.ensure(lc::reduce_scratch_bytes(n)));
+  int launches = 0;
+  unsigned int err = 0;
+  LC_CUDA(lc::cut_leaves_device(n, ctx->a.as<uint64_t>(), ctx->b.as<uint64_t>(), ctx->c.as<uint64_t>(),
+                                ctx->d.as<uint64_t>(), ctx->stats.as<uint64_t>(), max_passes, pass_stats, max_stats,
+                                n_passes, n_out, &err, ctx->scratch.p, ctx->stream, &launches));
+  g_launches += launches;
+  if (err) return reduce_error(err);
+  for (int k = 0; k < 5; ++k)
+    if (*n_out) LC_CUDA(cudaMemcpyAsync(host[k], cols[k]->p, *n_out * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  LC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LC_OK;
+}
+
+int lc_count_cycles(lc_ctx* ctx, uint64_t n, const uint64_t* src, const uint64_t* dst, const uint64_t* dist,
+                    const uint64_t* subtree_size, uint64_t* leader, uint64_t* hop_count, uint64_t* clock_length,
+                    uint64_t* tree_size, uint64_t* n_cycles) {
+  if (!ctx || !n_cycles) return fail(LC_ERR_ARG, "null argument");
+  *n_cycles = 0;
+  if (n == 0) return LC_OK;
+  LC_CUDA(cudaSetDevice(ctx->device));
+  const size_t nb = n * 8;
+  DevBuf* in[4] = {&ctx->a, &ctx->b, &ctx->c, &ctx->d};
+  const uint64_t* host[4] = {src, dst, dist, subtree_size};
+  for (int k = 0; k < 4; ++k) {
+    LC_CUDA(in[k]->ensure(nb));
+    LC_CUDA(cudaMemcpyAsync(in[k]->p, host[k], nb, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  LC_CUDA(ctx->stats.ensure(4 * nb));
+  uint64_t* out = ctx->stats.as<uint64_t>();
+  LC_CUDA(ctx->scratch.ensure(lc::cycles_scratch_bytes(n)));
+  int launches = 0;
+  unsigned int err = 0;
+  LC_CUDA(lc::count_cycles_device(n, ctx->a.as<uint64_t>(), ctx->b.as<uint64_t>(), ctx->c.as<uint64_t>(),
+                                  ctx->d.as<uint64_t>(), out, out + n, out + 2 * n, out + 3 * n, n_cycles, &err,
+                                  ctx->scratch.p, ctx->stream, &launches));
+  g_launches += launches;
+  if (err == 1) return fail(LC_ERR_NOT_PERMUTATION, "duplicate or unsorted source");
+  if (err) return reduce_error(err);
+  const uint64_t m = *n_cycles;
+  uint64_t* dsts[4] = {leader, hop_count, clock_length, tree_size};
+  for (int k = 0; k < 4; ++k)
+    if (m) LC_CUDA(cudaMemcpyAsync(dsts[k], out + k * n, m * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  LC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LC_OK;
+}
+
 }  // extern "C"

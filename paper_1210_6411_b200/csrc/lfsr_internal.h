@@ -85,6 +85,22 @@ int prune_blocks_per_sm(SpecId id);
 
 cudaError_t measure_lop3_peak(int sms, double* ops_per_s, double* sm_mhz);
 
+// Steps 4-5 (reduce.cu).  err_out: 0 ok, 1 unsorted sources, 2 not closed,
+// 3 destination not a source, 4 not a permutation.
+size_t reduce_scratch_bytes(uint64_t n);
+cudaError_t cut_leaves_device(uint64_t n, uint64_t* src, uint64_t* dst, uint64_t* dist, uint64_t* size,
+                              uint64_t* depth, uint32_t max_passes, uint64_t* pass_stats, uint32_t max_stats,
+                              uint32_t* n_passes, uint64_t* n_out, unsigned int* err_out, void* scratch,
+                              cudaStream_t st, int* launches);
+size_t cycles_scratch_bytes(uint64_t n);
+cudaError_t count_cycles_device(uint64_t n, const uint64_t* src, const uint64_t* dst, const uint64_t* dist,
+                                const uint64_t* size, uint64_t* leader, uint64_t* hops_out, uint64_t* clocks_out,
+                                uint64_t* tree_out, uint64_t* n_cycles, unsigned int* err_out, void* scratch,
+                                cudaStream_t st, int* launches);
+size_t sort_scratch_bytes(uint64_t n);
+cudaError_t sort_records_device(uint64_t n, uint64_t* const* cols, int ncols, void* scratch, size_t scratch_bytes,
+                                cudaStream_t st, int* launches);
+
 cudaError_t launch_first_missing(const uint64_t* set, uint64_t m, const uint64_t* q, uint64_t n,
                                  unsigned long long* first, cudaStream_t stream);
 

@@ -1,0 +1,112 @@
+"""GPU parity of the edge-output sort and steps 4-5 (leaf cutting, cycle counting)
+against the reference's own reduce.py run on mini skeletons (tests/golden/reduce.json)
+and, at larger sizes, the numpy restatement oracle/reduce_np.py."""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden_json, golden_npz
+
+pytestmark = pytest.mark.gpu
+
+
+def u64_digest(values):
+    return hashlib.sha256(np.asarray(values, dtype="<u8").tobytes()).hexdigest()
+
+
+def skeleton_edges(lc, specs, params, name, label):
+    spec, p = specs[name], params[name]
+    cands = lc.enumerate_candidates_array(spec, p)
+    if label == "dfs4":
+        skel, _ = lc.prune_shallow_segments(cands, lc.PruneConfig(mode="dfs", depth_limit=4), spec, p)
+    elif label == "bfs8":
+        skel, _ = lc.prune_shallow_segments(cands, lc.PruneConfig(mode="bfs", node_limit=8), spec, p)
+    else:
+        skel = cands.tolist()
+    return lc.build_skeleton_edges(skel, p, spec)
+
+
+@pytest.mark.parametrize("name", ["mini567", "mini789"])
+@pytest.mark.parametrize("label", ["full", "dfs4", "bfs8"])
+def test_pipeline_steps_1_to_5_match_reference(gpu, lc, specs, params, tmp_path, name, label):
+    want = golden_json("reduce.json")[f"{name}_{label}"]
+    edges = skeleton_edges(lc, specs, params, name, label)
+    assert len(edges) == want["skeleton"]
+    path = tmp_path / "edges.bin"
+    lc.write_edges(path, edges)
+    one = tmp_path / "one.bin"
+    st = lc.cut_leaves_pass(path, one, lc.ReduceConfig())
+    assert (st.leaves_removed, st.inner_nodes, st.out_size_sum) == tuple(
+        want["pass1"][k] for k in ("leaves_removed", "inner_nodes", "out_size_sum"))
+    assert u64_digest([v for r in lc.read_edges(one) for v in r]) == want["pass1"]["records_digest"]
+    fix = tmp_path / "fix.bin"
+    log = lc.cut_leaves_to_fixpoint(path, fix, lc.ReduceConfig())
+    assert [[p.leaves_removed, p.inner_nodes, p.out_size_sum] for p in log.passes] == want["passes"]
+    assert log.iterations == want["iterations"]
+    assert [list(r) for r in lc.read_edges(fix)] == want["fixpoint"]
+    assert [list(c) for c in lc.count_cycles(str(fix))] == want["cycles"]
+    assert [list(c) for c in lc.count_cycles(lc.read_edges(fix))] == want["cycles"]
+
+
+@pytest.mark.parametrize("name", ["mini567", "mini789"])
+def test_cycles_match_brute_force_oracle(gpu, lc, name):
+    """(hop count, clock length) per cycle == the reference oracle's exhaustive
+    functional-graph analysis (oracle.py:141-283)."""
+    fx = golden_json("reduce.json")
+    g = golden_npz(f"edges_{name}")
+    z = np.zeros(g["src"].size, dtype=np.uint64)
+    src, dst, dist, size, depth, _ = lc.cut_leaves_arrays(g["src"], g["dst"], g["dist"], z, z)
+    leader, hops, clocks, tree = lc.count_cycles_arrays(src, dst, dist, size)
+    assert sorted(zip(hops.tolist(), clocks.tolist())) == sorted(tuple(c) for c in fx[f"{name}_oracle_cycles"])
+    # conservation: every skeleton node is on a cycle or in a tree hanging off one
+    assert int(hops.sum()) + int(tree.sum()) == g["src"].size
+
+
+def test_sort_edge_arrays(gpu, lc):
+    rng = np.random.default_rng(1)
+    n = 300_000
+    src = rng.choice(np.uint64(1) << np.uint64(60), size=n, replace=False).astype(np.uint64)
+    dst = rng.integers(0, 1 << 62, size=n, dtype=np.uint64)
+    dist = np.arange(n, dtype=np.uint64)
+    s, d, w = lc.sort_edge_arrays(src, dst, dist)
+    order = np.argsort(src)
+    assert (s == src[order]).all() and (d == dst[order]).all() and (w == dist[order]).all()
+
+
+def test_random_functional_graph_matches_restatement(gpu, lc):
+    """2^20-node random mapping (mostly trees into few cycles) vs oracle/reduce_np.py."""
+    from oracle import reduce_np
+
+    rng = np.random.default_rng(7)
+    n = 1 << 20
+    src = np.sort(rng.choice(np.uint64(1) << np.uint64(40), size=n, replace=False).astype(np.uint64))
+    dst = src[rng.integers(0, n, size=n)]
+    dist = rng.integers(1, 1000, size=n, dtype=np.uint64)
+    z = np.zeros(n, dtype=np.uint64)
+    got = lc.cut_leaves_arrays(src, dst, dist, z, z)
+    want = reduce_np.cut_leaves(src, dst, dist, z, z)
+    assert got[5] == want[5]
+    for a, b in zip(got[:5], want[:5]):
+        assert (a == b).all()
+    cyc = lc.count_cycles_arrays(*got[:4])
+    assert [tuple(r) for r in zip(*(c.tolist() for c in cyc))] == reduce_np.count_cycles(*want[:4])
+
+
+def test_reduce_errors(gpu, lc, tmp_path):
+    # unsorted sources
+    with pytest.raises(ValueError):
+        lc.cut_leaves_arrays([5, 3], [3, 5], [1, 1], [0, 0], [0, 0])
+    # a leaf whose destination is no record: not closed
+    with pytest.raises(ValueError):
+        lc.cut_leaves_arrays([1, 2], [2, 9], [1, 1], [0, 0], [0, 0])
+    # trees left: not a permutation
+    with pytest.raises(lc.NotAPermutationError):
+        lc.count_cycles_arrays([1, 2, 3], [2, 3, 2], [1, 1, 1], [0, 0, 0])
+    with pytest.raises(lc.NotAPermutationError):
+        lc.count_cycles([lc.EdgeRecord(1, 2, 1, 0, 0), lc.EdgeRecord(1, 2, 1, 0, 0)])
+    with pytest.raises(ValueError):
+        lc.cut_leaves_pass(tmp_path / "x.bin", tmp_path / "y.bin", lc.ReduceConfig(memory_budget=1024))

@@ -129,3 +129,24 @@ def test_c1_sample_rows(specs):
     g = golden_npz("a51_c1_sample")
     d, w = port.walk(specs["a51"], 0x2AAA00, g["src"], stride=11_170_000)
     assert (d[:, 0] == g["dst"]).all() and (w[:, 0] == g["dist"]).all()
+
+
+@pytest.mark.skipif(not has_golden("reduce.json"), reason="reduce fixture not generated")
+def test_reduce_restatement_matches_reference(specs):
+    """oracle/reduce_np.py vs the reference's cut_leaves_pass iterated to the fixpoint
+    and count_cycles, on the full mini candidate sets."""
+    from oracle import reduce_np
+
+    fx = golden_json("reduce.json")
+    for name in ("mini567", "mini789"):
+        g = golden_npz(f"edges_{name}")
+        z = np.zeros(g["src"].size, dtype=np.uint64)
+        want = fx[f"{name}_full"]
+        out = reduce_np.cut_leaves(g["src"], g["dst"], g["dist"], z, z)
+        assert [list(p) for p in out[5]] == want["passes"]
+        fix = np.stack(out[:5], 1).tolist()
+        assert fix == want["fixpoint"]
+        assert [list(c) for c in reduce_np.count_cycles(*out[:4])] == want["cycles"]
+        one = reduce_np.cut_leaves(g["src"], g["dst"], g["dist"], z, z, max_passes=1)
+        assert list(one[5][0]) == [want["pass1"][k] for k in ("leaves_removed", "inner_nodes", "out_size_sum")]
+        assert u64_digest(np.stack(one[:5], 1).reshape(-1)) == want["pass1"]["records_digest"]
