@@ -34,7 +34,8 @@ def main():
     def instance(k, seed):
         rng = np.random.default_rng(seed)
         n = 1 << k
-        src = rng.choice(np.uint64(1) << np.uint64(63), size=n, replace=False).astype(np.uint64)
+        src = np.unique(rng.integers(0, 1 << 62, size=n + n // 64, dtype=np.uint64))[:n]
+        rng.shuffle(src)  # unsorted input: the edge-output sort has real work
         dst = src[rng.integers(0, n, size=n)]
         dist = rng.integers(11_000_000, 11_400_000, size=n, dtype=np.uint64)
         return src, dst, dist

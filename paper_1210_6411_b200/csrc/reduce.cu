@@ -14,6 +14,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "lfsr_internal.h"
@@ -54,34 +55,6 @@ __global__ void resolve_kernel(const uint64_t* __restrict__ src, uint64_t n, con
     }
     idx[i] = (lo < n && src[lo] == v) ? lo : kNone;
   }
-}
-
-__global__ void mark_kernel(const uint64_t* __restrict__ idx, uint64_t n, uint8_t* __restrict__ has_pred) {
-  GRID_STRIDE(i, n) {
-    const uint64_t j = idx[i];
-    if (j != kNone) has_pred[j] = 1;
-  }
-}
-
-// Leaves fold (size + 1, depth + 1) into their destination record.
-__global__ void fold_kernel(const uint64_t* __restrict__ idx, uint64_t n, const uint8_t* __restrict__ has_pred,
-                            unsigned long long* size, unsigned long long* depth,
-                            unsigned long long* leaves, unsigned int* err) {
-  uint32_t c = 0;
-  GRID_STRIDE(i, n) {
-    if (!has_pred[i]) {
-      ++c;
-      const uint64_t j = idx[i];
-      if (j == kNone) {
-        atomicExch(err, 2u);  // aggregate with no surviving record: input not closed
-      } else {
-        atomicAdd(&size[j], size[i] + 1ull);
-        atomicMax(&depth[j], depth[i] + 1ull);
-      }
-    }
-  }
-  c = __reduce_add_sync(0xffffffffu, c);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(leaves, static_cast<unsigned long long>(c));
 }
 
 __global__ void tile_count_kernel(const uint8_t* __restrict__ keep, uint64_t n, uint64_t* __restrict__ counts) {
@@ -152,11 +125,154 @@ __global__ void rank_kernel(const uint8_t* __restrict__ keep, uint64_t n, const 
   }
 }
 
+// ---- leaf-cutting pass kernels driven by device-side counts (so passes can be batched
+// in a CUDA graph without host round trips).  In-degree marks are pass stamps, so no
+// array has to be cleared between passes.
+struct PassCtl {
+  unsigned long long n;       // records in the current pass's input
+  unsigned long long pass;    // current pass number (1-based)
+  unsigned long long leaves;  // leaves removed by the current pass
+  unsigned long long sum;     // subtree-size sum over its survivors
+  unsigned long long done_at; // first pass that removed nothing (0: not yet)
+};
+
+__global__ void pass_begin_kernel(PassCtl* ctl) {
+  ctl->pass += 1;
+  ctl->leaves = 0;
+  ctl->sum = 0;
+}
+
+__global__ void mark_stamp_kernel(const uint64_t* __restrict__ idx, const PassCtl* __restrict__ ctl,
+                                  uint32_t* __restrict__ stamp) {
+  const uint64_t n = ctl->n;
+  const uint32_t p = static_cast<uint32_t>(ctl->pass);
+  GRID_STRIDE(i, n) {
+    const uint64_t j = idx[i];
+    if (j != kNone) stamp[j] = p;
+  }
+}
+
+__global__ void fold_stamp_kernel(const uint64_t* __restrict__ idx, PassCtl* ctl, const uint32_t* __restrict__ stamp,
+                                  unsigned long long* size, unsigned long long* depth, unsigned int* err) {
+  const uint64_t n = ctl->n;
+  const uint32_t p = static_cast<uint32_t>(ctl->pass);
+  uint32_t c = 0;
+  GRID_STRIDE(i, n) {
+    if (stamp[i] != p) {  // no record points here: a leaf
+      ++c;
+      const uint64_t j = idx[i];
+      if (j == kNone) {
+        atomicExch(err, 2u);  // aggregate with no surviving record: input not closed
+      } else {
+        atomicAdd(&size[j], size[i] + 1ull);
+        atomicMax(&depth[j], depth[i] + 1ull);
+      }
+    }
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&ctl->leaves, static_cast<unsigned long long>(c));
+}
+
+__global__ void tile_count_stamp_kernel(const uint32_t* __restrict__ stamp, const PassCtl* __restrict__ ctl,
+                                        uint64_t* __restrict__ counts) {
+  const uint64_t n = ctl->n;
+  const uint32_t p = static_cast<uint32_t>(ctl->pass);
+  const uint64_t tiles = (n + kTile - 1) / kTile;
+  __shared__ uint32_t part[kT / 32];
+  for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const uint64_t lo = t * kTile, hi = min(n, lo + kTile);
+    uint32_t c = 0;
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) c += stamp[i] == p ? 1u : 0u;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint64_t s = 0;
+      for (int w = 0; w < kT / 32; ++w) s += part[w];
+      counts[t] = s;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void tile_scan_dev_kernel(uint64_t* __restrict__ counts, const PassCtl* __restrict__ ctl) {
+  const uint64_t tiles = (ctl->n + kTile - 1) / kTile;
+  __shared__ uint64_t part[1024];
+  const uint64_t per = (tiles + blockDim.x - 1) / blockDim.x;
+  const uint64_t lo = threadIdx.x * per, hi = min(tiles, lo + per);
+  uint64_t sum = 0;
+  for (uint64_t i = lo; i < hi; ++i) sum += counts[i];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t run = 0;
+    for (uint32_t w = 0; w < blockDim.x; ++w) {
+      const uint64_t v = part[w];
+      part[w] = run;
+      run += v;
+    }
+    counts[tiles] = run;
+  }
+  __syncthreads();
+  uint64_t run = part[threadIdx.x];
+  for (uint64_t i = lo; i < hi; ++i) {
+    const uint64_t v = counts[i];
+    counts[i] = run;
+    run += v;
+  }
+}
+
+__global__ void rank_stamp_kernel(const uint32_t* __restrict__ stamp, const PassCtl* __restrict__ ctl,
+                                  const uint64_t* __restrict__ offsets, uint64_t* __restrict__ newpos) {
+  __shared__ uint32_t wcount[kT / 32];
+  const uint64_t n = ctl->n;
+  const uint32_t p = static_cast<uint32_t>(ctl->pass);
+  const uint64_t tiles = (n + kTile - 1) / kTile;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const uint64_t lo = t * kTile, hi = min(n, lo + kTile);
+    uint64_t pos = offsets[t];
+    for (uint64_t r = lo; r < hi; r += kT) {
+      const uint64_t i = r + threadIdx.x;
+      const bool k = i < hi && stamp[i] == p;
+      const uint32_t b = __ballot_sync(0xffffffffu, k);
+      if (lane == 0) wcount[warp] = __popc(b);
+      __syncthreads();
+      uint32_t before = 0, all = 0;
+#pragma unroll
+      for (int w = 0; w < kT / 32; ++w) {
+        const uint32_t v = wcount[w];
+        before += (static_cast<uint32_t>(w) < warp) ? v : 0u;
+        all += v;
+      }
+      if (i < hi) newpos[i] = k ? pos + before + __popc(b & ((1u << lane) - 1u)) : kNone;
+      pos += all;
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void pass_end_kernel(PassCtl* ctl, const uint64_t* __restrict__ counts, uint64_t* __restrict__ pstats,
+                                uint64_t max_stats) {
+  const uint64_t tiles = (ctl->n + kTile - 1) / kTile;
+  const uint64_t inner = counts[tiles];
+  const uint64_t p = ctl->pass;
+  if (p - 1 < max_stats) {
+    pstats[3 * (p - 1) + 0] = ctl->leaves;
+    pstats[3 * (p - 1) + 1] = inner;
+    pstats[3 * (p - 1) + 2] = ctl->sum;
+  }
+  if (ctl->leaves == 0 && ctl->done_at == 0) ctl->done_at = p;
+  ctl->n = inner;
+}
+
 struct Cols {
   uint64_t *src, *dst, *dist, *size, *depth, *idx;
 };
 
-__global__ void scatter_kernel(Cols in, Cols out, const uint64_t* __restrict__ newpos, uint64_t n) {
+__global__ void scatter_dev_kernel(Cols in, Cols out, const uint64_t* __restrict__ newpos,
+                                   const PassCtl* __restrict__ ctl) {
+  const uint64_t n = ctl->n;
   GRID_STRIDE(i, n) {
     const uint64_t p = newpos[i];
     if (p == kNone) continue;
@@ -170,11 +286,14 @@ __global__ void scatter_kernel(Cols in, Cols out, const uint64_t* __restrict__ n
   }
 }
 
-__global__ void sum_kernel(const uint64_t* __restrict__ v, uint64_t n, unsigned long long* out) {
+// subtree-size sum over the survivors (count = counts[tiles] of this pass)
+__global__ void sum_dev_kernel(const uint64_t* __restrict__ v, PassCtl* ctl, const uint64_t* __restrict__ counts) {
+  const uint64_t tiles = (ctl->n + kTile - 1) / kTile;
+  const uint64_t n = counts[tiles];
   uint64_t s = 0;
   GRID_STRIDE(i, n) { s += v[i]; }
   for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-  if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, static_cast<unsigned long long>(s));
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(&ctl->sum, static_cast<unsigned long long>(s));
 }
 
 // ------------------------------------------------------------------ cycles (step 5)
@@ -258,20 +377,56 @@ struct ReduceScratch {
 };
 
 size_t reduce_scratch_bytes(uint64_t n) {
-  // idx x2, the five columns (second copy), newpos, keep, tile counts, counters
+  // stamp (u32), newpos, idx x2, second set of five columns, tile counts, control, stats
   const uint64_t tiles = (n + kTile - 1) / kTile + 1;
-  return (8 * n * 8 + n + 1024) + tiles * 8 + 4096 + 16 * 256;
+  return n * 4 + 8 * n * 8 + tiles * 8 + 64 * 1024 + 16 * 256;
 }
 
+namespace {
+
+struct PassLaunch {
+  unsigned grid, tgrid;
+  PassCtl* ctl;
+  uint32_t* stamp;
+  uint64_t* tiles;
+  uint64_t* newpos;
+  uint64_t* pstats;
+  uint64_t max_stats;
+  unsigned int* err;
+};
+
+void launch_pass(const PassLaunch& L, const Cols& c, const Cols& o, cudaStream_t st) {
+  pass_begin_kernel<<<1, 1, 0, st>>>(L.ctl);
+  mark_stamp_kernel<<<L.grid, kT, 0, st>>>(c.idx, L.ctl, L.stamp);
+  fold_stamp_kernel<<<L.grid, kT, 0, st>>>(c.idx, L.ctl, L.stamp, reinterpret_cast<unsigned long long*>(c.size),
+                                           reinterpret_cast<unsigned long long*>(c.depth), L.err);
+  tile_count_stamp_kernel<<<L.tgrid, kT, 0, st>>>(L.stamp, L.ctl, L.tiles);
+  tile_scan_dev_kernel<<<1, 1024, 0, st>>>(L.tiles, L.ctl);
+  rank_stamp_kernel<<<L.tgrid, kT, 0, st>>>(L.stamp, L.ctl, L.tiles, L.newpos);
+  scatter_dev_kernel<<<L.grid, kT, 0, st>>>(c, o, L.newpos, L.ctl);
+  sum_dev_kernel<<<L.grid, kT, 0, st>>>(o.size, L.ctl, L.tiles);
+  pass_end_kernel<<<1, 1, 0, st>>>(L.ctl, L.tiles, L.pstats, L.max_stats);
+}
+
+constexpr int kLaunchesPerPass = 9;
+
+}  // namespace
+
+// Passes run back to back on the device: every kernel reads the current record count
+// and pass number from PassCtl, so the host only checks in every 32 passes (a CUDA graph
+// of two ping-pong passes replayed 16 times).  Passes after the fixpoint are no-ops
+// (nothing removed, every record kept), so overshooting is harmless.
 cudaError_t cut_leaves_device(uint64_t n, uint64_t* src, uint64_t* dst, uint64_t* dist, uint64_t* size,
                               uint64_t* depth, uint32_t max_passes, uint64_t* pass_stats, uint32_t max_stats,
                               uint32_t* n_passes, uint64_t* n_out, unsigned int* err_out, void* scratch,
                               cudaStream_t st, int* launches) {
   ReduceScratch s{static_cast<uint8_t*>(scratch), 0};
   unsigned int* err = s.take<unsigned int>(4);
-  unsigned long long* ctr = s.take<unsigned long long>(4);
+  PassCtl* ctl = s.take<PassCtl>(1);
+  const uint64_t stats_cap = max_stats ? max_stats : 1;
+  uint64_t* pstats = s.take<uint64_t>(3 * stats_cap);
   uint64_t* tiles_buf = s.take<uint64_t>((n + kTile - 1) / kTile + 1);
-  uint8_t* keep = s.take<uint8_t>(n + 1);
+  uint32_t* stamp = s.take<uint32_t>(n);
   uint64_t* newpos = s.take<uint64_t>(n);
   Cols a{src, dst, dist, size, depth, s.take<uint64_t>(n)};
   Cols b{s.take<uint64_t>(n), s.take<uint64_t>(n), s.take<uint64_t>(n), s.take<uint64_t>(n), s.take<uint64_t>(n),
@@ -280,11 +435,14 @@ cudaError_t cut_leaves_device(uint64_t n, uint64_t* src, uint64_t* dst, uint64_t
   *n_passes = 0;
   *n_out = n;
   *err_out = 0;
-  if ((e = cudaMemsetAsync(err, 0, 16, st)) != cudaSuccess) return e;
   if (n == 0) return cudaSuccess;
+  if ((e = cudaMemsetAsync(err, 0, 16, st)) != cudaSuccess) return e;
   check_sorted_kernel<<<grid_for(n), kT, 0, st>>>(src, n, err);
   resolve_kernel<<<grid_for(n), kT, 0, st>>>(src, n, dst, a.idx);
   *launches += 2;
+  if ((e = cudaMemsetAsync(stamp, 0, n * sizeof(uint32_t), st)) != cudaSuccess) return e;
+  const PassCtl init{n, 0, 0, 0, 0};
+  if ((e = cudaMemcpyAsync(ctl, &init, sizeof(init), cudaMemcpyHostToDevice, st)) != cudaSuccess) return e;
   unsigned int herr = 0;
   if ((e = cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
@@ -292,57 +450,62 @@ cudaError_t cut_leaves_device(uint64_t n, uint64_t* src, uint64_t* dst, uint64_t
     *err_out = herr;
     return cudaSuccess;
   }
-  uint64_t cur = n;
-  bool in_a = true;
-  for (uint32_t pass = 0; max_passes == 0 || pass < max_passes; ++pass) {
-    Cols& c = in_a ? a : b;
-    Cols& o = in_a ? b : a;
-    if ((e = cudaMemsetAsync(keep, 0, cur, st)) != cudaSuccess) return e;
-    if ((e = cudaMemsetAsync(ctr, 0, 32, st)) != cudaSuccess) return e;
-    mark_kernel<<<grid_for(cur), kT, 0, st>>>(c.idx, cur, keep);
-    fold_kernel<<<grid_for(cur), kT, 0, st>>>(c.idx, cur, keep, reinterpret_cast<unsigned long long*>(c.size),
-                                               reinterpret_cast<unsigned long long*>(c.depth), &ctr[0], err);
-    const uint64_t tiles = (cur + kTile - 1) / kTile;
-    tile_count_kernel<<<static_cast<unsigned>(tiles), kT, 0, st>>>(keep, cur, tiles_buf);
-    tile_scan_kernel<<<1, 1024, 0, st>>>(tiles_buf, tiles);
-    rank_kernel<<<static_cast<unsigned>(tiles), kT, 0, st>>>(keep, cur, tiles_buf, newpos);
-    scatter_kernel<<<grid_for(cur), kT, 0, st>>>(c, o, newpos, cur);
-    *launches += 6;
-    uint64_t h[2] = {0, 0};
-    if ((e = cudaMemcpyAsync(&h[0], &ctr[0], 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
-    if ((e = cudaMemcpyAsync(&h[1], &tiles_buf[tiles], 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+  const uint64_t tiles0 = (n + kTile - 1) / kTile;
+  PassLaunch L{std::min(grid_for(n), 4096u), static_cast<unsigned>(std::min<uint64_t>(tiles0, 4096)), ctl, stamp,
+               tiles_buf, newpos, pstats, max_stats, err};
+  PassCtl h{};
+  uint64_t executed = 0;
+  if (max_passes != 0) {
+    for (uint32_t k = 0; k < max_passes; ++k) {
+      launch_pass(L, (k & 1) ? b : a, (k & 1) ? a : b, st);
+      *launches += kLaunchesPerPass;
+    }
+    executed = max_passes;
+    if ((e = cudaMemcpyAsync(&h, ctl, sizeof(h), cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
     if ((e = cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
-    if (herr) {
-      *err_out = herr;
-      return cudaSuccess;
+  } else {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    if ((e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) return e;
+    launch_pass(L, a, b, st);
+    launch_pass(L, b, a, st);
+    if ((e = cudaStreamEndCapture(st, &graph)) != cudaSuccess) return e;
+    if ((e = cudaGraphInstantiate(&exec, graph, 0)) != cudaSuccess) return e;
+    constexpr int kBatch = 16;  // graphs (x2 passes) per host check-in
+    for (;;) {
+      for (int k = 0; k < kBatch; ++k)
+        if ((e = cudaGraphLaunch(exec, st)) != cudaSuccess) break;
+      if (e != cudaSuccess) break;
+      executed += 2 * kBatch;
+      *launches += 2 * kBatch * kLaunchesPerPass;
+      if ((e = cudaMemcpyAsync(&h, ctl, sizeof(h), cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+      if ((e = cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+      if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
+      if (herr || h.done_at) break;
     }
-    const uint64_t leaves = h[0], inner = h[1];
-    // sum of subtree sizes over the survivors (after folding)
-    sum_kernel<<<grid_for(inner), kT, 0, st>>>(o.size, inner, &ctr[1]);
-    *launches += 1;
-    uint64_t out_sum = 0;
-    if ((e = cudaMemcpyAsync(&out_sum, &ctr[1], 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
-    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
-    if (*n_passes < max_stats) {
-      pass_stats[3 * *n_passes + 0] = leaves;
-      pass_stats[3 * *n_passes + 1] = inner;
-      pass_stats[3 * *n_passes + 2] = out_sum;
-    }
-    ++*n_passes;
-    cur = inner;
-    in_a = !in_a;
-    if (leaves == 0) break;
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return e;
   }
-  // survivors back into the caller's columns (index column not returned)
-  if (!in_a) {
-    for (int k = 0; k < 5; ++k) {
-      uint64_t* from = (&b.src)[k];
-      uint64_t* to = (&a.src)[k];
-      if ((e = cudaMemcpyAsync(to, from, cur * 8, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
-    }
+  if (herr) {
+    *err_out = herr;
+    return cudaSuccess;
   }
-  *n_out = cur;
+  const uint64_t passes = h.done_at ? h.done_at : executed;
+  *n_passes = static_cast<uint32_t>(passes);
+  const uint64_t keep_stats = std::min<uint64_t>(passes, max_stats);
+  if (keep_stats)
+    if ((e = cudaMemcpyAsync(pass_stats, pstats, keep_stats * 3 * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+      return e;
+  // an odd number of executed passes leaves the survivors in the second column set
+  if (executed & 1) {
+    for (int k = 0; k < 5; ++k)
+      if ((e = cudaMemcpyAsync((&a.src)[k], (&b.src)[k], h.n * 8, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+        return e;
+  }
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  *n_out = h.n;
   return cudaSuccess;
 }
 
