@@ -599,7 +599,7 @@ int lc_cut_leaves(lc_ctx* ctx, uint64_t n, uint64_t* src, uint64_t* dst, uint64_
     LC_CUDA(cols[k]->ensure(nb));
     LC_CUDA(cudaMemcpyAsync(cols[k]->p, host[k], nb, cudaMemcpyHostToDevice, ctx->stream));
   }
-  LC_CUDA(ctx->scratch.ensure(lc::reduce_scratch_bytes(n)));
+  LC_CUDA(ctx->scratch.ensure(lc::reduce_scratch_bytes(n, max_stats)));
   int launches = 0;
   unsigned int err = 0;
   LC_CUDA(lc::cut_leaves_device(n, ctx->a.as<uint64_t>(), ctx->b.as<uint64_t>(), ctx->c.as<uint64_t>(),

@@ -87,7 +87,7 @@ cudaError_t measure_lop3_peak(int sms, double* ops_per_s, double* sm_mhz);
 
 // Steps 4-5 (reduce.cu).  err_out: 0 ok, 1 unsorted sources, 2 not closed,
 // 3 destination not a source, 4 not a permutation.
-size_t reduce_scratch_bytes(uint64_t n);
+size_t reduce_scratch_bytes(uint64_t n, uint32_t max_stats);
 cudaError_t cut_leaves_device(uint64_t n, uint64_t* src, uint64_t* dst, uint64_t* dist, uint64_t* size,
                               uint64_t* depth, uint32_t max_passes, uint64_t* pass_stats, uint32_t max_stats,
                               uint32_t* n_passes, uint64_t* n_out, unsigned int* err_out, void* scratch,

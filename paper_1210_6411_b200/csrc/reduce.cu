@@ -376,10 +376,10 @@ struct ReduceScratch {
   }
 };
 
-size_t reduce_scratch_bytes(uint64_t n) {
+size_t reduce_scratch_bytes(uint64_t n, uint32_t max_stats) {
   // stamp (u32), newpos, idx x2, second set of five columns, tile counts, control, stats
   const uint64_t tiles = (n + kTile - 1) / kTile + 1;
-  return n * 4 + 8 * n * 8 + tiles * 8 + 64 * 1024 + 16 * 256;
+  return n * 4 + 8 * n * 8 + tiles * 8 + 3ull * (max_stats + 1) * 8 + 64 * 1024 + 16 * 256;
 }
 
 namespace {

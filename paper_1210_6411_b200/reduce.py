@@ -128,7 +128,7 @@ def cut_leaves_arrays(src, dst, dist, subtree_size, subtree_depth, *, max_passes
     0: to the fixpoint.  Returns (src, dst, dist, size, depth, [(leaves, inner, out_size_sum)])."""
     cols = _cols(src, dst, dist, subtree_size, subtree_depth)
     n = cols[0].size
-    cap = 4096
+    cap = 1 << 16  # per-pass statistics kept (the paper's A5/1 skeleton needs 88 passes)
     stats = np.zeros((cap, 3), dtype=np.uint64)
     npass = C.c_uint32(0)
     nout = C.c_uint64(0)
