@@ -367,159 +367,11 @@ __device__ __forceinline__ int prune_step(uint64_t& x, uint64_t& d, uint64_t& ac
   return 0;
 }
 
-// Explicit-stack form of the same traversal (one expansion per node instead of the
-// stackless form's two plus a clock).  (P, R) is the node whose children are being
-// popped (at depth `top`) and its not-yet-popped children as a pattern mask, highest
-// pattern first = the reference's LIFO order.  Lower levels live in a level-tagged ring
-// in local memory; a level that fell out of the ring is recomputed exactly as in the
-// stackless form (parent = one forward clock, remaining siblings = lower patterns).
-// Every level below `top` was pushed by the current traversal, so a matching tag is
-// always the current candidate's entry -- no clearing between candidates.
-constexpr uint32_t kRing = 128;
-
-template <class S>
-__device__ __forceinline__ uint64_t child_of(uint64_t y, int q) {
-  const uint32_t r1 = static_cast<uint32_t>(y & S::M1);
-  const uint32_t r2 = static_cast<uint32_t>((y >> S::O2) & S::M2);
-  const uint32_t r3 = static_cast<uint32_t>((y >> S::O3) & S::M3);
-  const int p = clock_pattern(q);
-  const uint32_t p1 = (p & 1) ? unstep<S::L1, S::T1>(r1) : r1;
-  const uint32_t p2 = (p & 2) ? unstep<S::L2, S::T2>(r2) : r2;
-  const uint32_t p3 = (p & 4) ? unstep<S::L3, S::T3>(r3) : r3;
-  return static_cast<uint64_t>(p1) | (static_cast<uint64_t>(p2) << S::O2) | (static_cast<uint64_t>(p3) << S::O3);
-}
-
-struct RingTrav {
-  uint64_t P;
-  uint64_t acc;
-  uint32_t R;
-  uint32_t top;
-};
-
-// Root popped at depth 0.  Returns 0 running, 1 shallow (done), 2 deep (done).
-template <class S>
-__device__ __forceinline__ int ring_start(RingTrav& t, uint64_t root, uint32_t F, int mode, uint64_t limit) {
-  const Node<S> nd = expand_node<S>(root, F);
-  t.P = root;
-  t.R = nd.mask;
-  t.top = 0;
-  t.acc = (mode == 0 ? 0 : 1) + static_cast<uint64_t>(__popc(nd.mask));
-  if (nd.mask == 0u) return 1;
-  if (mode != 0 && t.acc > limit) {  // (dfs: depth-1 children never exceed a limit >= 1)
-    t.acc = limit + 1;
-    return 2;
-  }
-  return 0;
-}
-
-template <class S>
-__device__ __forceinline__ int ring_step(RingTrav& t, uint64_t* ringP, uint32_t* ringR, uint32_t* ringL,
-                                         uint32_t F, int mode, uint64_t limit) {
-  if (t.R == 0u) {  // P's subtree is done: back to its parent's level
-    if (t.top == 0u) return 1;
-    const uint32_t k = t.top - 1u, slot = k % kRing;
-    if (ringL[slot] == k + 1u) {
-      t.P = ringP[slot];
-      t.R = ringR[slot];
-    } else {
-      const uint64_t par = clock_scalar<S>(t.P);
-      const Node<S> nd = expand_node<S>(par, F);
-      uint32_t q = 0;
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (((nd.mask >> c) & 1u) && nd.child(c) == t.P) q = c;
-      t.P = par;
-      t.R = nd.mask & ((1u << q) - 1u);
-    }
-    t.top = k;
-    return 0;
-  }
-  const int q = 31 - __clz(t.R);
-  t.R &= ~(1u << q);
-  const uint64_t x = child_of<S>(t.P, q);
-  const Node<S> nd = expand_node<S>(x, F);
-  if (nd.mask != 0u) {
-    const uint32_t c = __popc(nd.mask);
-    if (mode == 0) {
-      if (t.top + 1u >= limit) {  // x sits at depth top+1; its children would exceed the limit
-        t.acc += 1;
-        return 2;
-      }
-      t.acc += c;
-    } else {
-      t.acc += c;
-      if (t.acc > limit) {
-        t.acc = limit + 1;
-        return 2;
-      }
-    }
-    const uint32_t slot = t.top % kRing;
-    ringP[slot] = t.P;
-    ringR[slot] = t.R;
-    ringL[slot] = t.top + 1u;
-    t.P = x;
-    t.R = nd.mask;
-    t.top += 1u;
-  }
-  return 0;
-}
-
 // Persistent: every lane runs its own traversal and takes the next candidate as soon as
 // it finishes (tickets aggregated over the lanes that need one), so a warp is never held
 // up by its deepest segment.
 template <class S>
 __global__ void __launch_bounds__(kThreads) prune_kernel(const uint64_t* __restrict__ cands, uint64_t n,
-                                                         uint32_t F, int mode, uint64_t limit,
-                                                         uint8_t* __restrict__ removed,
-                                                         uint64_t* __restrict__ work,
-                                                         unsigned long long* queue) {
-  const uint32_t lane = threadIdx.x & 31u;
-  uint64_t ringP[kRing];
-  uint32_t ringR[kRing], ringL[kRing];
-  RingTrav tr{0, 0, 0, 0};
-  uint64_t i = 0;
-  bool have = false, drained = false;
-  for (;;) {
-    if (!drained) {
-      const uint32_t need = __ballot_sync(kFull, !have);
-      if (need != 0u) {
-        const int leader = __ffs(need) - 1;
-        unsigned long long base = 0;
-        if (static_cast<int>(lane) == leader) base = atomicAdd(queue, static_cast<unsigned long long>(__popc(need)));
-        base = __shfl_sync(kFull, base, leader);
-        if (base + __popc(need) >= n) drained = true;
-        if (!have) {
-          i = base + __popc(need & ((1u << lane) - 1u));
-          if (i < n) {
-            const int r = ring_start<S>(tr, cands[i], F, mode, limit);
-            if (r != 0) {
-              removed[i] = r == 1 ? 1 : 0;
-              work[i] = tr.acc;
-            } else {
-              have = true;
-            }
-          }
-        }
-      }
-    }
-    if (!__any_sync(kFull, have)) {
-      if (drained) break;
-      continue;
-    }
-    if (have) {
-      const int r = ring_step<S>(tr, ringP, ringR, ringL, F, mode, limit);
-      if (r != 0) {
-        removed[i] = r == 1 ? 1 : 0;
-        work[i] = tr.acc;
-        have = false;
-      }
-    }
-  }
-}
-
-// Stackless variant (kept for reference and A/B measurement; not launched).
-template <class S>
-__global__ void __launch_bounds__(kThreads) prune_kernel_stackless(const uint64_t* __restrict__ cands, uint64_t n,
                                                          uint32_t F, int mode, uint64_t limit,
                                                          uint8_t* __restrict__ removed,
                                                          uint64_t* __restrict__ work,
