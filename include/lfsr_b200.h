@@ -98,8 +98,9 @@ void lc_launch_count_reset(void);
  * legs >= 1).  For every start, `legs` consecutive candidate hops; hop 1 is the first
  * candidate at clock >= max(stride, 1).  dest/dist are [n][legs] row-major.
  * max_clocks: the reference cap (bitslice.py:273-274); StrideError semantics in
- * DESIGN.md §"Cap".  refill: 0 = auto, 1 = refill a lane as soon as it finishes,
- * 1024 = refill a warp only when all its 1024 lanes are idle (near-constant walks).
+ * DESIGN.md §"Cap".  refill: 0 = auto (single-hop walks from all special-node-like
+ * starts refill whole warps, decided on the device; otherwise per lane), 1 = refill a
+ * lane as soon as it finishes, 1024 = refill a warp only when all 1024 lanes are idle.
  * hist_lo/hist_shift/hist_bins configure the chain-length histogram in `stats`
  * (LC_ST_HEADER + hist_bins + 2 words). */
 int lc_walk(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3, const uint64_t *starts,

@@ -245,8 +245,10 @@ int lc_walk_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const ui
   const uint64_t max_blocks = static_cast<uint64_t>(per_sm) * ctx->sms;
   const uint64_t want = (n + lanes_per_block - 1) / lanes_per_block;
   const int blocks = static_cast<int>(std::max<uint64_t>(1, std::min(max_blocks, want)));
-  uint32_t refill_min = refill;
-  if (refill_min == 0) refill_min = (legs == 1 && stride > 1) ? 1024u : 1u;
+  // auto (refill == 0): single-hop walks whose starts are all special-node-like run with
+  // whole-warp refill (decided on the device by the mode probe); everything else per lane
+  const bool auto_mode = refill == 0 && legs == 1;
+  const uint32_t refill_min = refill == 0 ? 1u : refill;
   // one queue per warp scheduler when the persistent grid covers every SM
   const uint32_t nq = (ctx->mapped_sms == ctx->sms && static_cast<uint64_t>(blocks) == max_blocks)
                           ? 4u * static_cast<uint32_t>(ctx->sms) : 1u;
@@ -261,6 +263,11 @@ int lc_walk_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const ui
   g_launches += 1;
   if (n == 0) return LC_OK;
   if (!d_starts || !d_dest || !d_dist) return fail(LC_ERR_ARG, "null buffer");
+  uint32_t* mode_word = reinterpret_cast<uint32_t*>(exhausted + 1);
+  if (auto_mode) {
+    LC_CUDA(lc::launch_mode_probe(id, d_starts, n, static_cast<uint32_t>(fixed_r3), mode_word, st));
+    g_launches += 1;
+  }
 
   lc::WalkParams p{};
   p.starts = d_starts;
@@ -282,6 +289,7 @@ int lc_walk_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const ui
   p.exhausted = exhausted;
   p.stats = reinterpret_cast<unsigned long long*>(d_stats);
   p.meta = ctx->meta.as<lc::LaneMeta>();
+  p.mode_word = auto_mode ? mode_word : nullptr;
   LC_CUDA(lc::launch_walk(id, static_f, p, blocks, st));
   g_launches += 1;
   return LC_OK;

@@ -44,6 +44,7 @@ struct WalkParams {
   unsigned int* exhausted;     // set once every queue is empty
   unsigned long long* stats;   // LC_ST_* block
   LaneMeta* meta;              // [threads][32]
+  const uint32_t* mode_word;   // auto mode: 1 = whole-warp refill, 0 = lane refill (else null)
 };
 
 // Launchers (defined in the .cu files); all enqueue on `stream`.
@@ -54,6 +55,10 @@ cudaError_t launch_init_stats(uint64_t* stats, uint64_t hist_lo, uint32_t hist_s
                               unsigned long long* queues, uint32_t nq, unsigned int* exhausted,
                               cudaStream_t stream);
 cudaError_t probe_smids(int sms, unsigned int* d_flags, cudaStream_t stream);
+// mode_word <- 1 iff every start is a special-node-like start (fixed R3, R3 clocked at
+// once): near-constant chain lengths, so whole-warp refill loses nothing.
+cudaError_t launch_mode_probe(SpecId id, const uint64_t* starts, uint64_t n, uint32_t F, uint32_t* mode_word,
+                              cudaStream_t stream);
 
 cudaError_t launch_is_candidate(SpecId id, const uint64_t* xs, uint64_t n, uint32_t F, uint8_t* out,
                                 cudaStream_t stream);

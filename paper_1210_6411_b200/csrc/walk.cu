@@ -158,7 +158,11 @@ struct WalkShared {
   unsigned long long t[kWalkThreads / 32];  // warp clock
   uint32_t own[kWalkThreads / 32];          // warp scheduler queue
   uint32_t open[kWalkThreads / 32];         // queues not yet exhausted for this warp
+  uint32_t warp_mode;                       // 1: whole-warp refill (1024-start items)
+  uint32_t refill_min;                      // lane mode: refill at this many idle lanes
 };
+
+constexpr uint32_t kWarpItem = 1024;  // starts per queue item in whole-warp mode
 
 template <class S, bool SF>
 __device__ __forceinline__ void whole_warp_refill(const WalkParams& p, volatile WalkShared& sh,
@@ -166,7 +170,7 @@ __device__ __forceinline__ void whole_warp_refill(const WalkParams& p, volatile 
   constexpr uint64_t kStateMask = S::NB >= 64 ? ~0ull : ((1ull << S::NB) - 1ull);
   const uint32_t tid = tid_x(), lane = tid & 31u, w = tid >> 5;
   const uint64_t gtid = static_cast<uint64_t>(ctaid_x()) * kWalkThreads + tid;
-  const uint64_t items = (p.n + p.chunk - 1) / p.chunk;
+  const uint64_t items = (p.n + kWarpItem - 1) / kWarpItem;
   const uint64_t t = sh.t[w];
   uint32_t qi = 0, got = 0;
   uint64_t b = 0;
@@ -179,7 +183,7 @@ __device__ __forceinline__ void whole_warp_refill(const WalkParams& p, volatile 
   }
   qi = __shfl_sync(kFull, qi, 0);
   b = __shfl_sync(kFull, b, 0);
-  const uint64_t base = ((b * p.nq) + qi) * p.chunk;
+  const uint64_t base = ((b * p.nq) + qi) * kWarpItem;
   const uint64_t wbase = gtid - lane;  // first thread of this warp
   bool all_safe = true;
   for (uint32_t r = 0; r < 32u; ++r) {
@@ -249,7 +253,7 @@ __device__ __forceinline__ void lane_refill(const WalkParams& p, volatile WalkSh
     const uint32_t idle = ~sh.active[tid];
     const uint32_t nidle = __popc(idle);
     const uint32_t widle = __reduce_add_sync(kFull, nidle);
-    if (widle == 0u || widle < p.refill_min) break;
+    if (widle == 0u || widle < sh.refill_min) break;
     uint32_t qi = 0, got = 0;
     uint64_t b = 0;
     if (lane == 0) got = take_items(p, items, sh.own[w], widle, &qi, &b);
@@ -399,7 +403,12 @@ __global__ void __launch_bounds__(kWalkThreads, LC_WALK_MIN_BLOCKS) walk_kernel(
       sh.t[w] = 0ull;
       sh.open[w] = 1u;
     }
-    __syncwarp();
+    if (tid == 0) {
+      const uint32_t warp_mode = p.mode_word ? *p.mode_word : (p.chunk > 1u ? 1u : 0u);
+      sh.warp_mode = warp_mode;
+      sh.refill_min = warp_mode ? kWarpItem : p.refill_min;
+    }
+    __syncthreads();
   }
 
   uint32_t s[S::NB];
@@ -415,7 +424,7 @@ __global__ void __launch_bounds__(kWalkThreads, LC_WALK_MIN_BLOCKS) walk_kernel(
     {
       const uint32_t tid = tid_x(), w = tid >> 5;
       if (sh.open[w]) {
-        if (p.chunk > 1u) {
+        if (sh.warp_mode) {
           if (__all_sync(kFull, sh.active[tid] == 0u)) whole_warp_refill<S, SF>(p, sh, s);
         } else {
           lane_refill<S, SF>(p, sh, s);
@@ -476,6 +485,24 @@ __global__ void smid_probe_kernel(unsigned int* flags) {
   if (threadIdx.x == 0) flags[smid & 1023u] = 1u;
 }
 
+// Auto refill mode: whole-warp refill iff every start is on the fixed plane with R3
+// clocked at once (the window-safe starts of a special-node walk).  *mode must be 1 on
+// entry; any other start clears it.
+template <class S>
+__global__ void mode_probe_kernel(const uint64_t* __restrict__ starts, uint64_t n, uint32_t F, uint32_t* mode) {
+  constexpr uint64_t kStateMask = S::NB >= 64 ? ~0ull : ((1ull << S::NB) - 1ull);
+  bool ok = true;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t x = starts[i] & kStateMask;
+    const uint32_t r1 = static_cast<uint32_t>(x & S::M1), r2 = static_cast<uint32_t>((x >> S::O2) & S::M2);
+    const uint32_t r3 = static_cast<uint32_t>((x >> S::O3) & S::M3);
+    const uint32_t c1 = (r1 >> S::CT1) & 1u, c2 = (r2 >> S::CT2) & 1u, c3 = (r3 >> S::CT3) & 1u;
+    ok = ok && r3 == F && (c3 == c1 || c3 == c2);
+  }
+  if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) *mode = 0u;
+}
+
 template <class S, bool SF>
 cudaError_t launch_t(const WalkParams& p, int blocks, cudaStream_t stream) {
   walk_kernel<S, SF><<<blocks, kWalkThreads, 0, stream>>>(p);
@@ -505,6 +532,22 @@ cudaError_t launch_init_stats(uint64_t* stats, uint64_t hist_lo, uint32_t hist_s
 
 cudaError_t probe_smids(int sms, unsigned int* d_flags, cudaStream_t stream) {
   smid_probe_kernel<<<sms * 16, 32, 0, stream>>>(d_flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mode_probe(SpecId id, const uint64_t* starts, uint64_t n, uint32_t F, uint32_t* mode_word,
+                              cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(mode_word, 0, sizeof(uint32_t), stream);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(mode_word, 1, 1, stream);  // little-endian: word = 1
+  if (e != cudaSuccess) return e;
+  const unsigned g = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 4096));
+  switch (id) {
+    case SpecId::A51: mode_probe_kernel<A51><<<g ? g : 1, 256, 0, stream>>>(starts, n, F, mode_word); break;
+    case SpecId::MINI567: mode_probe_kernel<MINI567><<<g ? g : 1, 256, 0, stream>>>(starts, n, F, mode_word); break;
+    case SpecId::MINI789: mode_probe_kernel<MINI789><<<g ? g : 1, 256, 0, stream>>>(starts, n, F, mode_word); break;
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 
