@@ -115,7 +115,7 @@ struct lc_ctx {
   int device = 0;
   int sms = 0;
   cudaStream_t stream = nullptr;
-  DevBuf meta, queue, stats, a, b, c, d, scratch, smmap, pq;
+  DevBuf meta, queue, stats, a, b, c, d, scratch, smmap, pq, pool_a, pool_b;
   int mapped_sms = -1;  // SMs found by the %smid probe (-1: not probed yet)
 };
 
@@ -181,7 +181,7 @@ int lc_ctx_destroy(lc_ctx* ctx) {
   if (!ctx) return LC_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  for (DevBuf* b : {&ctx->meta, &ctx->queue, &ctx->stats, &ctx->a, &ctx->b, &ctx->c, &ctx->d, &ctx->scratch, &ctx->smmap, &ctx->pq})
+  for (DevBuf* b : {&ctx->meta, &ctx->queue, &ctx->stats, &ctx->a, &ctx->b, &ctx->c, &ctx->d, &ctx->scratch, &ctx->smmap, &ctx->pq, &ctx->pool_a, &ctx->pool_b})
     b->release();
   cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -221,34 +221,31 @@ int lc_host_free(void* p) {
 
 // ------------------------------------------------------------------------- walks
 
-int lc_walk_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const uint64_t* d_starts,
-                   uint64_t n, uint64_t stride, uint64_t max_clocks, uint32_t legs, uint32_t refill,
-                   uint64_t* d_dest, uint64_t* d_dist, uint64_t hist_lo, uint32_t hist_shift,
-                   uint32_t hist_bins, uint64_t* d_stats, void* stream) {
-  if (!ctx) return fail(LC_ERR_ARG, "null context");
-  lc::SpecId id;
-  int rc = check_spec(spec, &id);
-  if (rc) return rc;
-  if ((rc = check_fixed(id, fixed_r3))) return rc;
-  if (stride < 1) return fail(LC_ERR_ARG, "stride must be >= 1");
-  if (legs < 1) return fail(LC_ERR_ARG, "legs must be >= 1");
-  if (hist_shift > 63) return fail(LC_ERR_ARG, "hist_shift must be < 64");
-  if (refill > 1024) return fail(LC_ERR_ARG, "refill must be in [0, 1024]");
-  if (!d_stats) return fail(LC_ERR_ARG, "stats buffer required");
-  LC_CUDA(cudaSetDevice(ctx->device));
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
-  if ((rc = ensure_smsp_map(ctx))) return rc;
+namespace {
 
-  const bool static_f = fixed_r3 == default_fixed(id);
-  const int per_sm = lc::walk_blocks_per_sm(id, static_f);
+struct WalkArgs {
+  lc::SpecId id;
+  uint64_t fixed_r3, stride, max_clocks, hist_lo;
+  uint32_t legs, refill, hist_shift, hist_bins;
+};
+
+// One walk launch.  resume != null: the items are parked lanes (lane mode, no stats
+// reset).  pool != null: drained warps park below park_below live lanes.
+int walk_launch(lc_ctx* ctx, const WalkArgs& a, const uint64_t* d_starts, const lc::ResumeRec* resume, uint64_t n,
+                uint64_t* d_dest, uint64_t* d_dist, uint64_t* d_stats, lc::ResumeRec* pool,
+                unsigned long long* pool_count, uint32_t park_below, cudaStream_t st) {
+  int rc = ensure_smsp_map(ctx);
+  if (rc) return rc;
+  const bool static_f = a.fixed_r3 == default_fixed(a.id);
+  const int per_sm = lc::walk_blocks_per_sm(a.id, static_f);
   const uint64_t lanes_per_block = lc::kWalkThreads * 32ull;
   const uint64_t max_blocks = static_cast<uint64_t>(per_sm) * ctx->sms;
   const uint64_t want = (n + lanes_per_block - 1) / lanes_per_block;
   const int blocks = static_cast<int>(std::max<uint64_t>(1, std::min(max_blocks, want)));
   // auto (refill == 0): single-hop walks whose starts are all special-node-like run with
   // whole-warp refill (decided on the device by the mode probe); everything else per lane
-  const bool auto_mode = refill == 0 && legs == 1;
-  const uint32_t refill_min = refill == 0 ? 1u : refill;
+  const bool auto_mode = resume == nullptr && a.refill == 0 && a.legs == 1;
+  const uint32_t refill_min = (resume || a.refill == 0) ? 1u : a.refill;
   // one queue per warp scheduler when the persistent grid covers every SM
   const uint32_t nq = (ctx->mapped_sms == ctx->sms && static_cast<uint64_t>(blocks) == max_blocks)
                           ? 4u * static_cast<uint32_t>(ctx->sms) : 1u;
@@ -259,13 +256,14 @@ int lc_walk_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const ui
   unsigned int* exhausted = reinterpret_cast<unsigned int*>(queues + static_cast<size_t>(nq) * 16);
 
   // stats header (counters zero, min = ~0, error index = ~0, histogram config), queues
-  LC_CUDA(lc::launch_init_stats(d_stats, hist_lo, hist_shift, hist_bins, queues, nq, exhausted, st));
+  LC_CUDA(lc::launch_init_stats(resume ? nullptr : d_stats, a.hist_lo, a.hist_shift, a.hist_bins, queues, nq,
+                                exhausted, st));
   g_launches += 1;
   if (n == 0) return LC_OK;
-  if (!d_starts || !d_dest || !d_dist) return fail(LC_ERR_ARG, "null buffer");
+  if ((!d_starts && !resume) || !d_dest || !d_dist) return fail(LC_ERR_ARG, "null buffer");
   uint32_t* mode_word = reinterpret_cast<uint32_t*>(exhausted + 1);
   if (auto_mode) {
-    LC_CUDA(lc::launch_mode_probe(id, d_starts, n, static_cast<uint32_t>(fixed_r3), mode_word, st));
+    LC_CUDA(lc::launch_mode_probe(a.id, d_starts, n, static_cast<uint32_t>(a.fixed_r3), mode_word, st));
     g_launches += 1;
   }
 
@@ -274,13 +272,13 @@ int lc_walk_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const ui
   p.n = n;
   p.dst = d_dest;
   p.dist = d_dist;
-  p.stride = stride;
-  p.cap1 = max_clocks == ~0ull ? ~0ull : max_clocks + 1;
-  p.hist_lo = hist_lo;
-  p.hist_shift = hist_shift;
-  p.hist_bins = hist_bins;
-  p.legs = legs;
-  p.fixed_r3 = static_cast<uint32_t>(fixed_r3);
+  p.stride = a.stride;
+  p.cap1 = a.max_clocks == ~0ull ? ~0ull : a.max_clocks + 1;
+  p.hist_lo = a.hist_lo;
+  p.hist_shift = a.hist_shift;
+  p.hist_bins = a.hist_bins;
+  p.legs = a.legs;
+  p.fixed_r3 = static_cast<uint32_t>(a.fixed_r3);
   p.refill_min = refill_min;
   p.chunk = refill_min >= 1024u ? 1024u : 1u;
   p.nq = nq;
@@ -290,17 +288,71 @@ int lc_walk_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const ui
   p.stats = reinterpret_cast<unsigned long long*>(d_stats);
   p.meta = ctx->meta.as<lc::LaneMeta>();
   p.mode_word = auto_mode ? mode_word : nullptr;
-  LC_CUDA(lc::launch_walk(id, static_f, p, blocks, st));
+  p.resume = resume;
+  p.pool = pool;
+  p.pool_count = pool_count;
+  p.park_below = pool ? park_below : 0u;
+  LC_CUDA(lc::launch_walk(a.id, static_f, p, blocks, st));
   g_launches += 1;
   return LC_OK;
 }
 
+int check_walk_args(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, uint64_t stride, uint32_t legs,
+                    uint32_t hist_shift, uint32_t refill, WalkArgs* a) {
+  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  int rc = check_spec(spec, &a->id);
+  if (rc) return rc;
+  if ((rc = check_fixed(a->id, fixed_r3))) return rc;
+  if (stride < 1) return fail(LC_ERR_ARG, "stride must be >= 1");
+  if (legs < 1) return fail(LC_ERR_ARG, "legs must be >= 1");
+  if (hist_shift > 63) return fail(LC_ERR_ARG, "hist_shift must be < 64");
+  if (refill > 1024) return fail(LC_ERR_ARG, "refill must be in [0, 1024]");
+  return LC_OK;
+}
+
+}  // namespace
+
+int lc_walk_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const uint64_t* d_starts,
+                   uint64_t n, uint64_t stride, uint64_t max_clocks, uint32_t legs, uint32_t refill,
+                   uint64_t* d_dest, uint64_t* d_dist, uint64_t hist_lo, uint32_t hist_shift,
+                   uint32_t hist_bins, uint64_t* d_stats, void* stream) {
+  WalkArgs a{};
+  int rc = check_walk_args(ctx, spec, fixed_r3, stride, legs, hist_shift, refill, &a);
+  if (rc) return rc;
+  if (!d_stats) return fail(LC_ERR_ARG, "stats buffer required");
+  a.fixed_r3 = fixed_r3;
+  a.stride = stride;
+  a.max_clocks = max_clocks;
+  a.hist_lo = hist_lo;
+  a.legs = legs;
+  a.refill = refill;
+  a.hist_shift = hist_shift;
+  a.hist_bins = hist_bins;
+  LC_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  return walk_launch(ctx, a, d_starts, nullptr, n, d_dest, d_dist, d_stats, nullptr, nullptr, 0, st);
+}
+
+// Host-buffer walk.  Runs in rounds: warps that drain below half occupancy park their
+// live lanes, and the next round resumes them packed densely, so the tail of wide-spread
+// walks does not run on mostly idle warps.  Parking is only enabled while a round has
+// more lanes than the GPU has warp schedulers x 1024 (below that, packing gains nothing).
 int lc_walk(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const uint64_t* starts, uint64_t n,
             uint64_t stride, uint64_t max_clocks, uint32_t legs, uint32_t refill, uint64_t* dest,
             uint64_t* dist, uint64_t hist_lo, uint32_t hist_shift, uint32_t hist_bins,
             uint64_t* stats) {
-  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  WalkArgs a{};
+  int rc = check_walk_args(ctx, spec, fixed_r3, stride, legs, hist_shift, refill, &a);
+  if (rc) return rc;
   if (!stats) return fail(LC_ERR_ARG, "stats buffer required");
+  a.fixed_r3 = fixed_r3;
+  a.stride = stride;
+  a.max_clocks = max_clocks;
+  a.hist_lo = hist_lo;
+  a.legs = legs;
+  a.refill = refill;
+  a.hist_shift = hist_shift;
+  a.hist_bins = hist_bins;
   LC_CUDA(cudaSetDevice(ctx->device));
   const size_t sb = (LC_ST_HEADER + hist_bins + 2ull) * sizeof(uint64_t);
   const size_t nb = static_cast<size_t>(n) * sizeof(uint64_t);
@@ -310,10 +362,36 @@ int lc_walk(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const uint64_t*
   LC_CUDA(ctx->c.ensure(std::max<size_t>(ob, 8)));
   LC_CUDA(ctx->stats.ensure(sb));
   if (n) LC_CUDA(cudaMemcpyAsync(ctx->a.p, starts, nb, cudaMemcpyHostToDevice, ctx->stream));
-  int rc = lc_walk_device(ctx, spec, fixed_r3, ctx->a.as<uint64_t>(), n, stride, max_clocks, legs, refill,
-                          ctx->b.as<uint64_t>(), ctx->c.as<uint64_t>(), hist_lo, hist_shift, hist_bins,
-                          ctx->stats.as<uint64_t>(), ctx->stream);
-  if (rc) return rc;
+  const uint64_t park_threshold = 4ull * static_cast<uint64_t>(ctx->sms) * 1024ull;  // lanes in a full wave of schedulers
+  const bool park = n > park_threshold;
+  lc::ResumeRec* pools[2] = {nullptr, nullptr};
+  unsigned long long* pcount = nullptr;
+  if (park) {
+    const size_t cap = std::min<uint64_t>(n, 8ull * park_threshold) * sizeof(lc::ResumeRec);
+    LC_CUDA(ctx->pool_a.ensure(cap));
+    LC_CUDA(ctx->pool_b.ensure(cap));
+    LC_CUDA(ctx->pq.ensure(16));
+    pools[0] = ctx->pool_a.as<lc::ResumeRec>();
+    pools[1] = ctx->pool_b.as<lc::ResumeRec>();
+    pcount = ctx->pq.as<unsigned long long>() + 1;
+  }
+  const lc::ResumeRec* resume = nullptr;
+  uint64_t round_n = n;
+  for (int round = 0;; ++round) {
+    lc::ResumeRec* out = park ? pools[round & 1] : nullptr;
+    const bool park_now = park && round_n > park_threshold;
+    if (park) LC_CUDA(cudaMemsetAsync(pcount, 0, 8, ctx->stream));
+    rc = walk_launch(ctx, a, ctx->a.as<uint64_t>(), resume, round_n, ctx->b.as<uint64_t>(), ctx->c.as<uint64_t>(),
+                     ctx->stats.as<uint64_t>(), park_now ? out : nullptr, pcount, 512u, ctx->stream);
+    if (rc) return rc;
+    if (!park_now) break;
+    unsigned long long parked = 0;
+    LC_CUDA(cudaMemcpyAsync(&parked, pcount, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    LC_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (parked == 0) break;
+    resume = out;
+    round_n = parked;
+  }
   LC_CUDA(cudaMemcpyAsync(stats, ctx->stats.p, sb, cudaMemcpyDeviceToHost, ctx->stream));
   LC_CUDA(cudaStreamSynchronize(ctx->stream));
   if (stats[LC_ST_ERROR]) {

@@ -23,6 +23,18 @@ struct LaneMeta {
   uint32_t pad;
 };
 
+// A parked lane (lane mode): state and leg bookkeeping relative to the parking clock, so
+// a later launch can resume it in any lane of any warp (csrc/walk.cu, "parking").
+struct ResumeRec {
+  uint64_t state;
+  uint64_t walk;
+  uint64_t elapsed;   // clocks since the leg started
+  uint64_t arm_rel;   // clocks until the lane may report (0: armed)
+  uint64_t dead_rel;  // clocks until the cap audit (kInf: none)
+  uint32_t legs_done;
+  uint32_t pad;
+};
+
 struct WalkParams {
   const uint64_t* starts;
   uint64_t n;
@@ -45,6 +57,11 @@ struct WalkParams {
   unsigned long long* stats;   // LC_ST_* block
   LaneMeta* meta;              // [threads][32]
   const uint32_t* mode_word;   // auto mode: 1 = whole-warp refill, 0 = lane refill (else null)
+  const ResumeRec* resume;     // lane mode: items are parked lanes instead of starts
+  ResumeRec* pool;             // parking destination (null: never park)
+  unsigned long long* pool_count;
+  uint32_t park_below;         // park a drained warp once fewer lanes than this are live
+  uint32_t pad2;
 };
 
 // Launchers (defined in the .cu files); all enqueue on `stream`.

@@ -277,6 +277,23 @@ __device__ __forceinline__ void lane_refill(const WalkParams& p, volatile WalkSh
     for (uint32_t todo = idle; todo != 0u && j_item < got; todo &= todo - 1u, ++j_item) {
       const int j = __ffs(todo) - 1;
       const uint64_t k = (b + j_item) * p.nq + qi;
+      if (p.resume) {
+        // a parked lane: same leg, clocks re-based on this warp's clock (mod 2^64)
+        const ResumeRec rec = p.resume[k];
+        insert_lane<S::NB>(s, j, rec.state);
+        LaneMeta m;
+        m.walk = rec.walk;
+        m.leg_start = t - rec.elapsed;
+        m.arm_at = sat_add(t, rec.arm_rel);
+        m.deadline = rec.dead_rel == kInf ? kInf : sat_add(t, rec.dead_rel);
+        m.legs_done = rec.legs_done;
+        m.pad = 0u;
+        meta[j] = m;
+        active |= 1u << j;
+        next_arm = min(next_arm, m.arm_at);
+        next_dead = min(next_dead, m.deadline);
+        continue;
+      }
       const uint64_t x = p.starts[k] & kStateMask;
       const uint32_t r1 = static_cast<uint32_t>(x & S::M1);
       const uint32_t r2 = static_cast<uint32_t>((x >> S::O2) & S::M2);
@@ -305,6 +322,44 @@ __device__ __forceinline__ void lane_refill(const WalkParams& p, volatile WalkSh
     sh.next_dead[tid] = next_dead;
     if (raise_pending(p)) break;
   }
+}
+
+// Lane parking: once the queues are drained, a warp whose live lanes fall below
+// park_below exports them (state + leg bookkeeping relative to its clock) to the pool and
+// retires; the host relaunches on the pool with the lanes packed densely, so warps stay
+// full through the tail of wide-spread walks (random starts, several hops).
+template <class S>
+__device__ __forceinline__ void park_lanes(const WalkParams& p, volatile WalkShared& sh, const uint32_t (&s)[S::NB]) {
+  const uint32_t tid = tid_x(), lane = tid & 31u, w = tid >> 5;
+  const uint64_t gtid = static_cast<uint64_t>(ctaid_x()) * kWalkThreads + tid;
+  const LaneMeta* const meta = p.meta + gtid * 32u;
+  const uint64_t t = sh.t[w];
+  const uint32_t act = sh.active[tid], armed = sh.armed[tid];
+  const uint32_t cnt = __popc(act);
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(kFull, incl, o);
+    if (lane >= static_cast<uint32_t>(o)) incl += v;
+  }
+  unsigned long long base = 0;
+  if (lane == 31u) base = atomicAdd(p.pool_count, static_cast<unsigned long long>(incl));
+  base = __shfl_sync(kFull, base, 31) + (incl - cnt);
+  for (uint32_t a = act; a != 0u; a &= a - 1u, ++base) {
+    const int j = __ffs(a) - 1;
+    const LaneMeta m = meta[j];
+    ResumeRec r;
+    r.state = extract_lane<S::NB>(s, j);
+    r.walk = m.walk;
+    r.elapsed = t - m.leg_start;
+    r.arm_rel = ((armed >> j) & 1u) || m.arm_at <= t ? 0ull : m.arm_at - t;
+    r.dead_rel = m.deadline == kInf ? kInf : (m.deadline > t ? m.deadline - t : 0ull);
+    r.legs_done = m.legs_done;
+    r.pad = 0u;
+    p.pool[base] = r;
+  }
+  sh.active[tid] = 0u;
+  __syncwarp();
 }
 
 // Events at the warp clock (rare): special nodes, arming, cap audits.
@@ -434,6 +489,11 @@ __global__ void __launch_bounds__(kWalkThreads, LC_WALK_MIN_BLOCKS) walk_kernel(
         if (!sh.open[w]) break;
         continue;
       }
+      if (p.pool && !sh.open[w] &&
+          __reduce_add_sync(kFull, static_cast<uint32_t>(__popc(sh.active[tid]))) < p.park_below) {
+        park_lanes<S>(p, sh, s);
+        break;
+      }
       // ---- next warp-wide event horizon
       const uint64_t t = sh.t[w];
       const uint64_t h = min(sh.next_arm[tid], sh.next_dead[tid]);
@@ -466,7 +526,7 @@ __global__ void init_stats_kernel(unsigned long long* st, uint64_t hist_lo, uint
   const uint64_t words = LC_ST_HEADER + hist_bins + 2ull;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  for (uint64_t i = i0; i < words; i += stride) {
+  for (uint64_t i = i0; st && i < words; i += stride) {  // st null: queues only (resume round)
     unsigned long long v = 0;
     if (i == LC_ST_MIN || i == LC_ST_ERROR_INDEX) v = ~0ull;
     else if (i == LC_ST_HIST_LO) v = hist_lo;
