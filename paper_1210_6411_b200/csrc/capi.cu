@@ -485,11 +485,9 @@ int lc_enumerate_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, uin
     return fail(LC_ERR_ARG, "R2 rows must satisfy 1 <= r2_lo <= r2_hi <= 2^%d", l2);
   LC_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
-  const uint64_t words = lc::enumerate_scratch_words(id, r2_lo, r2_hi);
-  LC_CUDA(ctx->scratch.ensure(words * 8));
   int launches = 0;
-  LC_CUDA(lc::launch_enumerate(id, static_cast<uint32_t>(fixed_r3), r2_lo, r2_hi, d_out, cap, d_count,
-                               ctx->scratch.as<uint64_t>(), words, st, &launches));
+  LC_CUDA(lc::launch_enumerate(id, static_cast<uint32_t>(fixed_r3), r2_lo, r2_hi, d_out, cap, d_count, st,
+                               &launches));
   g_launches += launches;
   return LC_OK;
 }

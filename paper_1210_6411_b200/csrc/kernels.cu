@@ -433,9 +433,6 @@ inline unsigned grid_for(uint64_t n, int threads, uint64_t per_thread = 1) {
   return static_cast<unsigned>(g == 0 ? 1 : (g > (1u << 20) ? (1u << 20) : g));
 }
 
-template <template <class> class K>
-struct Dispatch;
-
 }  // namespace
 
 #define LC_DISPATCH(id, ...)                                  \
@@ -464,17 +461,8 @@ cudaError_t launch_clock(SpecId id, const uint64_t* xs, uint64_t n, uint64_t t, 
   LC_DISPATCH(id, clock_kernel<S><<<g == 0 ? 1 : g, 128, 0, stream>>>(xs, n, t, out); return cudaGetLastError());
 }
 
-uint64_t enumerate_scratch_words(SpecId id, uint64_t r2_lo, uint64_t r2_hi) {
-  uint64_t m1 = id == SpecId::A51 ? A51::M1 : (id == SpecId::MINI567 ? MINI567::M1 : MINI789::M1);
-  const uint64_t total = (r2_hi > r2_lo ? r2_hi - r2_lo : 0) * m1;
-  return (total + kTile - 1) / kTile + 1;
-}
-
 cudaError_t launch_enumerate(SpecId id, uint32_t F, uint64_t r2_lo, uint64_t r2_hi, uint64_t* out,
-                             uint64_t cap, uint64_t* d_count, uint64_t* scratch,
-                             uint64_t scratch_words, cudaStream_t stream, int* launches) {
-  (void)scratch;
-  (void)scratch_words;
+                             uint64_t cap, uint64_t* d_count, cudaStream_t stream, int* launches) {
   const uint64_t rows = r2_hi > r2_lo ? r2_hi - r2_lo : 0;
   const unsigned grid = static_cast<unsigned>(rows == 0 ? 1 : (rows > (1u << 20) ? (1u << 20) : rows));
   if (launches) *launches += 1;

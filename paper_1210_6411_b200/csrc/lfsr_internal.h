@@ -84,16 +84,11 @@ cudaError_t launch_predecessors(SpecId id, const uint64_t* xs, uint64_t n, uint6
 cudaError_t launch_clock(SpecId id, const uint64_t* xs, uint64_t n, uint64_t t, uint64_t* out,
                          cudaStream_t stream);
 
-// Ordered compaction generators (enumeration and the seeded start set).
-struct EnumRange {
-  uint64_t r2_lo;
-  uint64_t rows;
-};
-// Counts per tile then writes; scratch must hold tiles+1 u64.  Returns tiles used.
+// Step-1 enumeration of R2 rows [r2_lo, r2_hi) (closed-form streaming writer).
 cudaError_t launch_enumerate(SpecId id, uint32_t F, uint64_t r2_lo, uint64_t r2_hi, uint64_t* out,
-                             uint64_t cap, uint64_t* d_count, uint64_t* scratch,
-                             uint64_t scratch_words, cudaStream_t stream, int* launches);
-uint64_t enumerate_scratch_words(SpecId id, uint64_t r2_lo, uint64_t r2_hi);
+                             uint64_t cap, uint64_t* d_count, cudaStream_t stream, int* launches);
+// K0 seeded start set: ordered compaction (tile counts, scan, ballot writes); scratch
+// must hold random_scratch_words(trials) u64.
 cudaError_t launch_random_candidates(SpecId id, uint32_t F, uint64_t seed, uint64_t trials,
                                      uint64_t* out, uint64_t cap, uint64_t* d_count,
                                      uint64_t* scratch, uint64_t scratch_words,
