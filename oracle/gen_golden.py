@@ -350,6 +350,35 @@ def gen_reduce(ref):
     save_json("reduce.json", out)
 
 
+def gen_tuning(ref):
+    """auto_depth_limit (pipeline.py:313-333) and calibrate_stride (bitslice.py:357-376)
+    outputs, and PruneConfig validation outcomes (pipeline.py:65-84)."""
+    C, P, B = ref.cipher, ref.pipeline, ref.bitslice
+    table = C.build_predecessor_table()
+    out = {}
+    for spec, sample, seed in ((C.MINI567, 256, 0), (C.MINI789, 256, 3), (C.A51, 24, 0), (C.A51, 256, 0)):
+        params = C.CandidateParams.from_spec(spec, C.default_fixed_r3(spec))
+        t0 = time.time()
+        out[f"auto_depth_{spec.name}_{sample}_{seed}"] = P.auto_depth_limit(spec, params, table, sample=sample,
+                                                                            seed=seed)
+        print(spec.name, "auto_depth_limit", out[f"auto_depth_{spec.name}_{sample}_{seed}"], f"{time.time() - t0:.1f}s")
+    for spec in (C.MINI567, C.MINI789):
+        params = C.CandidateParams.from_spec(spec, C.default_fixed_r3(spec))
+        for n, sd in ((300, 5), (1000, 7)):
+            out[f"calibrate_{spec.name}_{n}_{sd}"] = B.calibrate_stride(spec, params, table, samples=n, seed=sd)
+    cfgs = {}
+    for mode, d, nl, w in (("dfs", None, None, 1), ("dfs", 0, None, 1), ("dfs", 127, None, 1), ("dfs", 126, None, 1),
+                           ("bfs", None, 10, 1), ("bfs", None, 127, 1), ("bfs", None, 0, 1), ("xyz", 3, 3, 1),
+                           ("dfs", 3, None, 0)):
+        try:
+            P.PruneConfig(mode=mode, depth_limit=d, node_limit=nl, workers=w).validate(C.MINI567)
+            cfgs[f"{mode}_{d}_{nl}_{w}"] = "ok"
+        except ValueError:
+            cfgs[f"{mode}_{d}_{nl}_{w}"] = "ValueError"
+    out["prune_config_mini567"] = cfgs
+    save_json("tuning.json", out)
+
+
 def c1_starts(ref, n):
     C, P = ref.cipher, ref.pipeline
     table = C.build_predecessor_table()
@@ -435,6 +464,8 @@ def main():
         gen_kat(ref)
     elif what == "reduce":
         gen_reduce(ref)
+    elif what == "tuning":
+        gen_tuning(ref)
     elif what == "c1":
         gen_c1(ref, int(sys.argv[2]) if len(sys.argv) > 2 else os.cpu_count())
     else:

@@ -131,3 +131,30 @@ def test_k0_matches_numpy_restatement(gpu, lc, specs, params, name):
     want = k0.random_candidates(specs[name], params[name].fixed_r3, 12345, 5000)
     assert (got == want).all()
     assert lc.is_candidate(got, params[name], specs[name]).all()
+
+
+def test_tuning_functions_match_reference(gpu, lc, specs, params):
+    """auto_depth_limit (pipeline.py:313-333, GPU batched segment probes) and
+    calibrate_stride (bitslice.py:357-376, GPU two-hop walks) return the reference's values."""
+    fx = golden_json("tuning.json")
+    for key, want in fx.items():
+        if key.startswith("auto_depth_"):
+            _, _, name, sample, seed = key.split("_")
+            got = lc.auto_depth_limit(specs[name], params[name], sample=int(sample), seed=int(seed))
+            assert got == want, key
+        elif key.startswith("calibrate_"):
+            _, name, n, seed = key.split("_")
+            assert lc.calibrate_stride(specs[name], params[name], samples=int(n), seed=int(seed)) == want, key
+    # the reference's sampled stride for mini567 (SURVEY.md §4: 149 / 150, unsafe > 148)
+    meta = golden_json("edges_mini567.json")["calibrate_stride"]
+    assert lc.calibrate_stride(specs["mini567"], params["mini567"], samples=500, seed=0) == meta["500_0"]
+    assert lc.calibrate_stride(specs["mini567"], params["mini567"], samples=2000, seed=1) == meta["2000_1"]
+    assert lc.calibrate_stride(specs["a51"], params["a51"]) == lc.DEFAULT_STRIDE_A51
+
+
+def test_edges_chunk_worker(gpu, lc, specs, params):
+    from paper_1210_6411_b200.pipeline import _edges_chunk
+
+    g = golden_npz("edges_mini789")
+    rows = _edges_chunk((g["src"][:500].tolist(), params["mini789"], specs["mini789"], None, 1))
+    assert rows == list(zip(g["src"][:500].tolist(), g["dst"][:500].tolist(), g["dist"][:500].tolist()))

@@ -221,3 +221,17 @@ def test_stats_combine_and_summary():
     summ = stats_summary(whole)
     assert summ["edges"] == 1000 and abs(summ["mean"] - d.mean()) < 1e-6
     assert abs(summ["sd"] - d.astype(np.float64).std()) < 1e-3
+
+
+def test_prune_config_validation_matches_reference(lc):
+    fx = golden_json("tuning.json")["prune_config_mini567"]
+    for key, want in fx.items():
+        mode, d, nl, w = key.split("_")
+        cfg = lc.PruneConfig(mode=mode, depth_limit=None if d == "None" else int(d),
+                             node_limit=None if nl == "None" else int(nl), workers=int(w))
+        try:
+            cfg.validate(lc.MINI567)
+            got = "ok"
+        except ValueError:
+            got = "ValueError"
+        assert got == want, key
