@@ -76,14 +76,12 @@ __device__ void record_edge(const WalkParams& p, uint64_t d) {
 template <class S>
 __device__ __forceinline__ void run_unchecked(uint32_t (&s)[S::NB], uint32_t n) {
 #pragma unroll 1
-  for (uint32_t k = n >> 2; k != 0; --k) {
-    step<S>(s);
-    step<S>(s);
-    step<S>(s);
-    step<S>(s);
+  for (uint32_t k = n >> 3; k != 0; --k) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) step<S>(s);
   }
 #pragma unroll 1
-  for (uint32_t k = n & 3u; k != 0; --k) step<S>(s);
+  for (uint32_t k = n & 7u; k != 0; --k) step<S>(s);
 }
 
 // Steps until a special node shows up in an armed lane of the warp (returns the number
