@@ -13,7 +13,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "liblfsr_b200.so")
+LIB_PATH = os.environ.get("LFSR_LIB") or os.path.join(_HERE, "_lib", "liblfsr_b200.so")  # override: A/B builds
 
 LC_OK = 0
 LC_ERR_ARG = -1
