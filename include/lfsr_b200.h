@@ -178,6 +178,35 @@ int lc_cut_leaves(lc_ctx *ctx, uint64_t n, uint64_t *src, uint64_t *dst, uint64_
                   uint64_t *subtree_size, uint64_t *subtree_depth, uint32_t max_passes,
                   uint64_t *pass_stats, uint32_t max_stats, uint32_t *n_passes, uint64_t *n_out);
 
+/* lc_cut_leaves on device-resident columns (synchronous on `stream`; NULL = legacy
+ * default stream).  pass_stats is a host array. */
+int lc_cut_leaves_device(lc_ctx *ctx, uint64_t n, uint64_t *d_src, uint64_t *d_dst, uint64_t *d_dist,
+                         uint64_t *d_subtree_size, uint64_t *d_subtree_depth, uint32_t max_passes,
+                         uint64_t *pass_stats, uint32_t max_stats, uint32_t *n_passes, uint64_t *n_out,
+                         void *stream);
+
+/* Sharded leaf cutting: the multi-GPU form of cut_leaves_pass / cut_leaves_to_fixpoint
+ * (reduce.py:118-223).  Rank r of n_ranks holds the records whose sources fall in its
+ * contiguous range (rank_first[r] = its first source, rank_count[r] = its record count;
+ * ranges ascend with r) in device columns it owns.  The host driver alternates
+ *   emit(phase) -> exchange messages by owner rank (all-to-all) -> apply(phase)
+ * once with phase 0 (in-degree counting) and then once per pass with phase 1 (fold the
+ * pass's leaves into their destinations).  A message is 3 u64 words (destination,
+ * size + 1, depth + 1); emit writes them to `d_send` (capacity 3 * n words) grouped by
+ * owner rank and returns the per-rank counts in counts[n_ranks] and, in info[2], the
+ * records emitted (phase 1: this pass's local leaves) and the shard's error word
+ * (2: a destination has no record -- input not closed).  finish compacts the survivors
+ * in place (*n_out of them, source order).  All calls are synchronous on `stream`. */
+typedef struct lc_cut_shard lc_cut_shard;
+int lc_cut_shard_create(lc_ctx *ctx, uint64_t n, uint64_t *d_src, uint64_t *d_dst, uint64_t *d_dist,
+                        uint64_t *d_subtree_size, uint64_t *d_subtree_depth, uint32_t n_ranks,
+                        const uint64_t *rank_first, const uint64_t *rank_count, void *stream,
+                        lc_cut_shard **out, uint64_t *size_sum);
+int lc_cut_shard_emit(lc_cut_shard *shard, int phase, uint64_t *d_send, uint64_t *counts, uint64_t *info);
+int lc_cut_shard_apply(lc_cut_shard *shard, int phase, const uint64_t *d_recv, uint64_t n_messages);
+int lc_cut_shard_finish(lc_cut_shard *shard, uint64_t *n_out);
+int lc_cut_shard_destroy(lc_cut_shard *shard);
+
 /* Replaces reduce.count_cycles (reduce.py:226-266): cycles of a permutation, sorted by
  * leader (smallest source on the cycle): hop count, clock length (sum of distances),
  * aggregate tree size (sum of subtree sizes).  Output arrays hold up to n entries. */

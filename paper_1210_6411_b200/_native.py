@@ -83,6 +83,14 @@ _SIGNATURES = {
     "lc_sort_edges": ([_vp, C.c_uint64, _u64p, _u64p, _u64p, _u64p, _u64p], C.c_int),
     "lc_cut_leaves": ([_vp, C.c_uint64, _u64p, _u64p, _u64p, _u64p, _u64p, C.c_uint32, _u64p, C.c_uint32,
                        C.POINTER(C.c_uint32), _u64p], C.c_int),
+    "lc_cut_leaves_device": ([_vp, C.c_uint64, _vp, _vp, _vp, _vp, _vp, C.c_uint32, _u64p, C.c_uint32,
+                              C.POINTER(C.c_uint32), _u64p, _vp], C.c_int),
+    "lc_cut_shard_create": ([_vp, C.c_uint64, _vp, _vp, _vp, _vp, _vp, C.c_uint32, _u64p, _u64p, _vp,
+                             C.POINTER(C.c_void_p), _u64p], C.c_int),
+    "lc_cut_shard_emit": ([_vp, C.c_int, _vp, _u64p, _u64p], C.c_int),
+    "lc_cut_shard_apply": ([_vp, C.c_int, _vp, C.c_uint64], C.c_int),
+    "lc_cut_shard_finish": ([_vp, _u64p], C.c_int),
+    "lc_cut_shard_destroy": ([_vp], C.c_int),
     "lc_count_cycles": ([_vp, C.c_uint64, _u64p, _u64p, _u64p, _u64p, _u64p, _u64p, _u64p, _u64p, _u64p],
                         C.c_int),
 }

@@ -697,6 +697,121 @@ int lc_cut_leaves(lc_ctx* ctx, uint64_t n, uint64_t* src, uint64_t* dst, uint64_
   return LC_OK;
 }
 
+int lc_cut_leaves_device(lc_ctx* ctx, uint64_t n, uint64_t* src, uint64_t* dst, uint64_t* dist,
+                         uint64_t* subtree_size, uint64_t* subtree_depth, uint32_t max_passes, uint64_t* pass_stats,
+                         uint32_t max_stats, uint32_t* n_passes, uint64_t* n_out, void* stream) {
+  if (!ctx || !n_passes || !n_out) return fail(LC_ERR_ARG, "null argument");
+  *n_passes = 0;
+  *n_out = n;
+  if (n == 0) return LC_OK;
+  if (!src || !dst || !dist || !subtree_size || !subtree_depth) return fail(LC_ERR_ARG, "null buffer");
+  if (max_stats && !pass_stats) return fail(LC_ERR_ARG, "null pass_stats");
+  LC_CUDA(cudaSetDevice(ctx->device));
+  // The passes are replayed from a CUDA graph, which cannot be captured on the legacy
+  // default stream: wait for the caller's stream, then run on the context's own stream
+  // (the call is synchronous, so the caller's later work sees the results).
+  LC_CUDA(cudaStreamSynchronize(stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy));
+  LC_CUDA(ctx->scratch.ensure(lc::reduce_scratch_bytes(n, max_stats)));
+  int launches = 0;
+  unsigned int err = 0;
+  LC_CUDA(lc::cut_leaves_device(n, src, dst, dist, subtree_size, subtree_depth, max_passes, pass_stats, max_stats,
+                                n_passes, n_out, &err, ctx->scratch.p, ctx->stream, &launches));
+  g_launches += launches;
+  return err ? reduce_error(err) : LC_OK;
+}
+
+}  // extern "C"
+
+struct lc_cut_shard {
+  lc_ctx* ctx = nullptr;
+  cudaStream_t stream = nullptr;
+  void* mem = nullptr;
+  lc::ShardState st{};
+};
+
+extern "C" {
+
+int lc_cut_shard_create(lc_ctx* ctx, uint64_t n, uint64_t* src, uint64_t* dst, uint64_t* dist,
+                        uint64_t* subtree_size, uint64_t* subtree_depth, uint32_t n_ranks,
+                        const uint64_t* rank_first, const uint64_t* rank_count, void* stream, lc_cut_shard** out,
+                        uint64_t* size_sum) {
+  if (!ctx || !out || !size_sum || !rank_first || !rank_count) return fail(LC_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (n_ranks == 0 || n_ranks > lc::kMaxShardRanks)
+    return fail(LC_ERR_ARG, "n_ranks must be in [1, %u]", lc::kMaxShardRanks);
+  if (n && (!src || !dst || !dist || !subtree_size || !subtree_depth)) return fail(LC_ERR_ARG, "null buffer");
+  // shard ranges must ascend (non-empty ranks only; the driver checks the last/first pairs)
+  uint64_t prev = 0;
+  bool any = false;
+  for (uint32_t r = 0; r < n_ranks; ++r) {
+    if (!rank_count[r]) continue;
+    if (any && rank_first[r] <= prev) return fail(LC_ERR_UNSORTED, "shard ranges do not ascend with rank");
+    prev = rank_first[r];
+    any = true;
+  }
+  LC_CUDA(cudaSetDevice(ctx->device));
+  lc_cut_shard* h = new lc_cut_shard;
+  h->ctx = ctx;
+  h->stream = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  cudaError_t e = cudaMalloc(&h->mem, lc::shard_scratch_bytes(n, n_ranks));
+  if (e != cudaSuccess) {
+    delete h;
+    return fail(LC_ERR_CUDA, "shard scratch: %s", cudaGetErrorString(e));
+  }
+  uint64_t* cols[5] = {src, dst, dist, subtree_size, subtree_depth};
+  unsigned int err = 0;
+  int launches = 0;
+  e = lc::shard_init(&h->st, h->mem, n, cols, n_ranks, rank_first, rank_count, size_sum, &err, h->stream, &launches);
+  g_launches += launches;
+  if (e != cudaSuccess || err) {
+    cudaFree(h->mem);
+    delete h;
+    if (e != cudaSuccess) return fail(LC_ERR_CUDA, "shard init: %s", cudaGetErrorString(e));
+    return reduce_error(err);
+  }
+  *out = h;
+  return LC_OK;
+}
+
+int lc_cut_shard_emit(lc_cut_shard* h, int phase, uint64_t* send, uint64_t* counts, uint64_t* info) {
+  if (!h || !counts || !info || (h->st.n && !send)) return fail(LC_ERR_ARG, "null argument");
+  if (phase != 0 && phase != 1) return fail(LC_ERR_ARG, "phase must be 0 or 1");
+  LC_CUDA(cudaSetDevice(h->ctx->device));
+  int launches = 0;
+  LC_CUDA(lc::shard_emit(&h->st, phase, send, counts, info, h->stream, &launches));
+  g_launches += launches;
+  return LC_OK;
+}
+
+int lc_cut_shard_apply(lc_cut_shard* h, int phase, const uint64_t* recv, uint64_t m) {
+  if (!h || (m && !recv)) return fail(LC_ERR_ARG, "null argument");
+  if (phase != 0 && phase != 1) return fail(LC_ERR_ARG, "phase must be 0 or 1");
+  LC_CUDA(cudaSetDevice(h->ctx->device));
+  int launches = 0;
+  LC_CUDA(lc::shard_apply(&h->st, phase, recv, m, h->stream, &launches));
+  g_launches += launches;
+  return LC_OK;
+}
+
+int lc_cut_shard_finish(lc_cut_shard* h, uint64_t* n_out) {
+  if (!h || !n_out) return fail(LC_ERR_ARG, "null argument");
+  LC_CUDA(cudaSetDevice(h->ctx->device));
+  int launches = 0;
+  unsigned int err = 0;
+  LC_CUDA(lc::shard_finish(&h->st, n_out, &err, h->stream, &launches));
+  g_launches += launches;
+  return err ? reduce_error(err) : LC_OK;
+}
+
+int lc_cut_shard_destroy(lc_cut_shard* h) {
+  if (!h) return LC_OK;
+  cudaSetDevice(h->ctx->device);
+  cudaStreamSynchronize(h->stream);
+  if (h->mem) cudaFree(h->mem);
+  delete h;
+  return LC_OK;
+}
+
 int lc_count_cycles(lc_ctx* ctx, uint64_t n, const uint64_t* src, const uint64_t* dst, const uint64_t* dist,
                     const uint64_t* subtree_size, uint64_t* leader, uint64_t* hop_count, uint64_t* clock_length,
                     uint64_t* tree_size, uint64_t* n_cycles) {

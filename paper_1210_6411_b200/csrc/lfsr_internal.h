@@ -109,6 +109,46 @@ cudaError_t cut_leaves_device(uint64_t n, uint64_t* src, uint64_t* dst, uint64_t
                               uint64_t* depth, uint32_t max_passes, uint64_t* pass_stats, uint32_t max_stats,
                               uint32_t* n_passes, uint64_t* n_out, unsigned int* err_out, void* scratch,
                               cudaStream_t st, int* launches);
+
+// Leaf-cutting control block in device memory (frontier sizes and pass counters, so
+// passes can be replayed from a CUDA graph).
+struct CutCtl {
+  unsigned long long cnt[2];   // frontier sizes; pass parity w consumes cnt[w], fills cnt[w^1]
+  unsigned long long alive;    // records alive before the current pass
+  unsigned long long sum;      // subtree-size sum over the alive records
+  unsigned long long pass;     // passes completed
+  unsigned long long done_at;  // first pass that removed nothing (0: not yet)
+};
+
+// One rank's shard of a sharded leaf cut (multi-GPU step 4): contiguous source range,
+// caller-owned device columns, in-degrees, alive flags and two frontiers in scratch.
+struct ShardState {
+  uint64_t n;
+  uint64_t* cols[5];  // source, destination, distance, subtree_size, subtree_depth
+  uint32_t n_ranks, nb;
+  uint64_t* bounds;   // [nb] first source per non-empty rank (bounds[0] = 0)
+  uint32_t* brank;    // [nb] rank of each bound
+  unsigned long long *ocount, *ocursor;
+  unsigned int* err;
+  CutCtl* ctl;
+  uint64_t* tiles;
+  unsigned int* indeg;
+  uint8_t* alive;
+  uint64_t* f[2];
+  int w;
+  bool started;
+};
+size_t shard_scratch_bytes(uint64_t n, uint32_t n_ranks);
+cudaError_t shard_init(ShardState* sh, void* scratch, uint64_t n, uint64_t* const cols[5], uint32_t n_ranks,
+                       const uint64_t* rank_first, const uint64_t* rank_count, uint64_t* size_sum,
+                       unsigned int* err_out, cudaStream_t st, int* launches);
+cudaError_t shard_emit(ShardState* sh, int phase, uint64_t* send, uint64_t* counts, uint64_t* info,
+                       cudaStream_t st, int* launches);
+cudaError_t shard_apply(ShardState* sh, int phase, const uint64_t* msgs, uint64_t m, cudaStream_t st,
+                        int* launches);
+cudaError_t shard_finish(ShardState* sh, uint64_t* n_out, unsigned int* err_out, cudaStream_t st, int* launches);
+constexpr uint32_t kMaxShardRanks = 1024;
+
 size_t cycles_scratch_bytes(uint64_t n);
 cudaError_t count_cycles_device(uint64_t n, const uint64_t* src, const uint64_t* dst, const uint64_t* dist,
                                 const uint64_t* size, uint64_t* leader, uint64_t* hops_out, uint64_t* clocks_out,

@@ -125,175 +125,222 @@ __global__ void rank_kernel(const uint8_t* __restrict__ keep, uint64_t n, const 
   }
 }
 
-// ---- leaf-cutting pass kernels driven by device-side counts (so passes can be batched
-// in a CUDA graph without host round trips).  In-degree marks are pass stamps, so no
-// array has to be cleared between passes.
-struct PassCtl {
-  unsigned long long n;       // records in the current pass's input
-  unsigned long long pass;    // current pass number (1-based)
-  unsigned long long leaves;  // leaves removed by the current pass
-  unsigned long long sum;     // subtree-size sum over its survivors
-  unsigned long long done_at; // first pass that removed nothing (0: not yet)
-};
+// ---- leaf cutting (step 4) as a frontier computation.  A record is a leaf of pass p iff
+// no record alive after pass p-1 points at it, i.e. its in-degree among alive records is
+// zero.  Removing the leaves of pass p decrements their destinations' in-degrees; the
+// records that reach zero are exactly the leaves of pass p+1.  So each pass touches only
+// its own leaves (total work O(n) over all passes instead of O(n) per pass), and the
+// (size + 1, depth + 1) folds are order-independent atomics (sum, max), which keeps the
+// result deterministic although frontier order is not.  Pass statistics need no scans:
+// with L_p leaves, inner_nodes = alive - L_p and the survivors' subtree-size sum grows by
+// exactly L_p (each leaf's size moves into its destination, plus one for the leaf).
 
-__global__ void pass_begin_kernel(PassCtl* ctl) {
-  ctl->pass += 1;
-  ctl->leaves = 0;
-  ctl->sum = 0;
+// Loop whose index base is shared by the 32 lanes of a warp, so warp collectives inside
+// see every lane (lanes past the end run with an out-of-range index).
+#define WARP_STRIDE(i0, n)                                                                 \
+  for (uint64_t i0 = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) & ~31ull; \
+       i0 < (n); i0 += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+
+// Warp-aggregated append: one atomic per warp.  All 32 lanes must call it.
+__device__ __forceinline__ void warp_append(bool push, uint64_t value, uint64_t* __restrict__ list,
+                                            unsigned long long* count) {
+  const uint32_t m = __ballot_sync(0xffffffffu, push);
+  if (m == 0) return;
+  const uint32_t lane = threadIdx.x & 31u;
+  const int leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if (static_cast<int>(lane) == leader) base = atomicAdd(count, static_cast<unsigned long long>(__popc(m)));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (push) list[base + __popc(m & ((1u << lane) - 1u))] = value;
 }
 
-__global__ void mark_stamp_kernel(const uint64_t* __restrict__ idx, const PassCtl* __restrict__ ctl,
-                                  uint32_t* __restrict__ stamp) {
-  const uint64_t n = ctl->n;
-  const uint32_t p = static_cast<uint32_t>(ctl->pass);
+__device__ __forceinline__ uint64_t find_source(const uint64_t* __restrict__ src, uint64_t n, uint64_t v) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (src[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < n && src[lo] == v) ? lo : kNone;
+}
+
+__global__ void indeg_count_kernel(const uint64_t* __restrict__ idx, uint64_t n, unsigned int* __restrict__ indeg) {
   GRID_STRIDE(i, n) {
     const uint64_t j = idx[i];
-    if (j != kNone) stamp[j] = p;
+    if (j != kNone) atomicAdd(&indeg[j], 1u);
   }
 }
 
-__global__ void fold_stamp_kernel(const uint64_t* __restrict__ idx, PassCtl* ctl, const uint32_t* __restrict__ stamp,
-                                  unsigned long long* size, unsigned long long* depth, unsigned int* err) {
-  const uint64_t n = ctl->n;
-  const uint32_t p = static_cast<uint32_t>(ctl->pass);
-  uint32_t c = 0;
-  GRID_STRIDE(i, n) {
-    if (stamp[i] != p) {  // no record points here: a leaf
-      ++c;
-      const uint64_t j = idx[i];
-      if (j == kNone) {
-        atomicExch(err, 2u);  // aggregate with no surviving record: input not closed
-      } else {
-        atomicAdd(&size[j], size[i] + 1ull);
-        atomicMax(&depth[j], depth[i] + 1ull);
-      }
-    }
-  }
-  c = __reduce_add_sync(0xffffffffu, c);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&ctl->leaves, static_cast<unsigned long long>(c));
-}
-
-__global__ void tile_count_stamp_kernel(const uint32_t* __restrict__ stamp, const PassCtl* __restrict__ ctl,
-                                        uint64_t* __restrict__ counts) {
-  const uint64_t n = ctl->n;
-  const uint32_t p = static_cast<uint32_t>(ctl->pass);
-  const uint64_t tiles = (n + kTile - 1) / kTile;
-  __shared__ uint32_t part[kT / 32];
-  for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-    const uint64_t lo = t * kTile, hi = min(n, lo + kTile);
-    uint32_t c = 0;
-    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) c += stamp[i] == p ? 1u : 0u;
-    c = __reduce_add_sync(0xffffffffu, c);
-    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint64_t s = 0;
-      for (int w = 0; w < kT / 32; ++w) s += part[w];
-      counts[t] = s;
-    }
-    __syncthreads();
+__global__ void frontier_init_kernel(const unsigned int* __restrict__ indeg, uint64_t n, uint64_t* __restrict__ f,
+                                     unsigned long long* cnt) {
+  WARP_STRIDE(i0, n) {
+    const uint64_t i = i0 + (threadIdx.x & 31u);
+    warp_append(i < n && indeg[i] == 0u, i, f, cnt);
   }
 }
 
-__global__ void tile_scan_dev_kernel(uint64_t* __restrict__ counts, const PassCtl* __restrict__ ctl) {
-  const uint64_t tiles = (ctl->n + kTile - 1) / kTile;
-  __shared__ uint64_t part[1024];
-  const uint64_t per = (tiles + blockDim.x - 1) / blockDim.x;
-  const uint64_t lo = threadIdx.x * per, hi = min(tiles, lo + per);
-  uint64_t sum = 0;
-  for (uint64_t i = lo; i < hi; ++i) sum += counts[i];
-  part[threadIdx.x] = sum;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint64_t run = 0;
-    for (uint32_t w = 0; w < blockDim.x; ++w) {
-      const uint64_t v = part[w];
-      part[w] = run;
-      run += v;
-    }
-    counts[tiles] = run;
-  }
-  __syncthreads();
-  uint64_t run = part[threadIdx.x];
-  for (uint64_t i = lo; i < hi; ++i) {
-    const uint64_t v = counts[i];
-    counts[i] = run;
-    run += v;
-  }
-}
-
-__global__ void rank_stamp_kernel(const uint32_t* __restrict__ stamp, const PassCtl* __restrict__ ctl,
-                                  const uint64_t* __restrict__ offsets, uint64_t* __restrict__ newpos) {
-  __shared__ uint32_t wcount[kT / 32];
-  const uint64_t n = ctl->n;
-  const uint32_t p = static_cast<uint32_t>(ctl->pass);
-  const uint64_t tiles = (n + kTile - 1) / kTile;
-  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-    const uint64_t lo = t * kTile, hi = min(n, lo + kTile);
-    uint64_t pos = offsets[t];
-    for (uint64_t r = lo; r < hi; r += kT) {
-      const uint64_t i = r + threadIdx.x;
-      const bool k = i < hi && stamp[i] == p;
-      const uint32_t b = __ballot_sync(0xffffffffu, k);
-      if (lane == 0) wcount[warp] = __popc(b);
-      __syncthreads();
-      uint32_t before = 0, all = 0;
-#pragma unroll
-      for (int w = 0; w < kT / 32; ++w) {
-        const uint32_t v = wcount[w];
-        before += (static_cast<uint32_t>(w) < warp) ? v : 0u;
-        all += v;
-      }
-      if (i < hi) newpos[i] = k ? pos + before + __popc(b & ((1u << lane) - 1u)) : kNone;
-      pos += all;
-      __syncthreads();
-    }
-  }
-}
-
-__global__ void pass_end_kernel(PassCtl* ctl, const uint64_t* __restrict__ counts, uint64_t* __restrict__ pstats,
-                                uint64_t max_stats) {
-  const uint64_t tiles = (ctl->n + kTile - 1) / kTile;
-  const uint64_t inner = counts[tiles];
-  const uint64_t p = ctl->pass;
-  if (p - 1 < max_stats) {
-    pstats[3 * (p - 1) + 0] = ctl->leaves;
-    pstats[3 * (p - 1) + 1] = inner;
-    pstats[3 * (p - 1) + 2] = ctl->sum;
-  }
-  if (ctl->leaves == 0 && ctl->done_at == 0) ctl->done_at = p;
-  ctl->n = inner;
-}
-
-struct Cols {
-  uint64_t *src, *dst, *dist, *size, *depth, *idx;
-};
-
-__global__ void scatter_dev_kernel(Cols in, Cols out, const uint64_t* __restrict__ newpos,
-                                   const PassCtl* __restrict__ ctl) {
-  const uint64_t n = ctl->n;
-  GRID_STRIDE(i, n) {
-    const uint64_t p = newpos[i];
-    if (p == kNone) continue;
-    out.src[p] = in.src[i];
-    out.dst[p] = in.dst[i];
-    out.dist[p] = in.dist[i];
-    out.size[p] = in.size[i];
-    out.depth[p] = in.depth[i];
-    const uint64_t j = in.idx[i];
-    out.idx[p] = j == kNone ? kNone : newpos[j];
-  }
-}
-
-// subtree-size sum over the survivors (count = counts[tiles] of this pass)
-__global__ void sum_dev_kernel(const uint64_t* __restrict__ v, PassCtl* ctl, const uint64_t* __restrict__ counts) {
-  const uint64_t tiles = (ctl->n + kTile - 1) / kTile;
-  const uint64_t n = counts[tiles];
+__global__ void sum_kernel(const uint64_t* __restrict__ v, uint64_t n, unsigned long long* out) {
   uint64_t s = 0;
   GRID_STRIDE(i, n) { s += v[i]; }
   for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-  if ((threadIdx.x & 31) == 0 && s) atomicAdd(&ctl->sum, static_cast<unsigned long long>(s));
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, static_cast<unsigned long long>(s));
+}
+
+// Remove the leaves of the current pass (frontier fcur) and fold them into their
+// destinations; destinations whose in-degree drops to zero form the next frontier.
+__global__ void cut_fold_kernel(CutCtl* ctl, int w, const uint64_t* __restrict__ fcur, uint64_t* __restrict__ fnext,
+                                const uint64_t* __restrict__ idx, unsigned long long* size,
+                                unsigned long long* depth, unsigned int* indeg, uint8_t* __restrict__ alive,
+                                unsigned int* err) {
+  const uint64_t m = ctl->cnt[w];
+  WARP_STRIDE(k0, m) {
+    const uint64_t k = k0 + (threadIdx.x & 31u);
+    bool push = false;
+    uint64_t j = kNone;
+    if (k < m) {
+      const uint64_t i = fcur[k];
+      alive[i] = 0;
+      j = idx[i];
+      if (j == kNone) {
+        atomicExch(err, 2u);  // aggregate with no surviving record: input not closed
+      } else {
+        atomicAdd(&size[j], size[i] + 1ull);  // i is a leaf: nothing folds into it this pass
+        atomicMax(&depth[j], depth[i] + 1ull);
+        push = atomicSub(&indeg[j], 1u) == 1u;
+      }
+    }
+    warp_append(push, j, fnext, &ctl->cnt[w ^ 1]);
+  }
+}
+
+__global__ void cut_pass_end_kernel(CutCtl* ctl, int w, uint64_t* __restrict__ pstats, uint64_t max_stats) {
+  const unsigned long long leaves = ctl->cnt[w];
+  const unsigned long long p = ++ctl->pass;
+  if (p - 1 < max_stats) {
+    pstats[3 * (p - 1) + 0] = leaves;
+    pstats[3 * (p - 1) + 1] = ctl->alive - leaves;
+    pstats[3 * (p - 1) + 2] = ctl->sum + leaves;
+  }
+  ctl->alive -= leaves;
+  ctl->sum += leaves;
+  ctl->cnt[w] = 0;
+  if (leaves == 0 && ctl->done_at == 0) ctl->done_at = p;
+}
+
+// ---- sharded leaf cutting (multi-GPU step 4).  Each rank holds one contiguous source
+// range; a record's destination may live on any rank, so in-degree counts and folds travel
+// as 3-word messages (destination, size + 1, depth + 1) grouped by owner rank, exchanged
+// with one all-to-all per pass by the host driver, and applied by the owner, which
+// resolves the destination by binary search over its own sources.
+
+__device__ __forceinline__ uint32_t owner_of(uint64_t v, const uint64_t* __restrict__ bounds,
+                                             const uint32_t* __restrict__ brank, uint32_t nb) {
+  uint32_t lo = 0, hi = nb;  // one past the last entry with bounds[e] <= v (bounds[0] == 0)
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (bounds[mid] <= v) lo = mid + 1;
+    else hi = mid;
+  }
+  return brank[lo - 1];
+}
+
+struct EmitArgs {
+  int phase;                    // 0: in-degree messages for every record, 1: the frontier's folds
+  uint64_t n;                   // records (phase 0)
+  const CutCtl* ctl;            // frontier count (phase 1)
+  int w;                        // current frontier parity
+  const uint64_t* frontier;
+  const uint64_t* dst;
+  const unsigned long long* size;
+  const unsigned long long* depth;
+  uint8_t* alive;
+  const uint64_t* bounds;
+  const uint32_t* brank;
+  uint32_t nb, n_ranks;
+  unsigned long long* ocount;   // [n_ranks] messages per owner
+  unsigned long long* ocursor;  // [n_ranks]
+  uint64_t* msgs;               // [3 * items], grouped by owner rank
+};
+
+__device__ __forceinline__ uint64_t emit_items(const EmitArgs& a) { return a.phase ? a.ctl->cnt[a.w] : a.n; }
+
+__global__ void emit_count_kernel(EmitArgs a) {
+  __shared__ unsigned int h[kMaxShardRanks];
+  for (uint32_t r = threadIdx.x; r < a.n_ranks; r += blockDim.x) h[r] = 0;
+  __syncthreads();
+  const uint64_t m = emit_items(a);
+  GRID_STRIDE(k, m) {
+    const uint64_t i = a.phase ? a.frontier[k] : k;
+    atomicAdd(&h[owner_of(a.dst[i], a.bounds, a.brank, a.nb)], 1u);
+  }
+  __syncthreads();
+  for (uint32_t r = threadIdx.x; r < a.n_ranks; r += blockDim.x)
+    if (h[r]) atomicAdd(&a.ocount[r], static_cast<unsigned long long>(h[r]));
+}
+
+__global__ void emit_write_kernel(EmitArgs a) {
+  __shared__ unsigned long long off[kMaxShardRanks];
+  if (threadIdx.x == 0) {
+    unsigned long long run = 0;
+    for (uint32_t r = 0; r < a.n_ranks; ++r) {
+      off[r] = run;
+      run += a.ocount[r];
+    }
+  }
+  __syncthreads();
+  const uint64_t m = emit_items(a);
+  const uint32_t lane = threadIdx.x & 31u;
+  WARP_STRIDE(k0, m) {
+    const uint64_t k = k0 + lane;
+    const bool valid = k < m;
+    uint64_t i = 0;
+    uint32_t o = 0xffffffffu;
+    if (valid) {
+      i = a.phase ? a.frontier[k] : k;
+      o = owner_of(a.dst[i], a.bounds, a.brank, a.nb);
+    }
+    // one cursor atomic per (warp, owner) group
+    const uint32_t peers = __match_any_sync(0xffffffffu, o);
+    const int leader = __ffs(peers) - 1;
+    unsigned long long base = 0;
+    if (valid && static_cast<int>(lane) == leader)
+      base = atomicAdd(&a.ocursor[o], static_cast<unsigned long long>(__popc(peers)));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (valid) {
+      const uint64_t slot = off[o] + base + __popc(peers & ((1u << lane) - 1u));
+      uint64_t* q = a.msgs + 3 * slot;
+      q[0] = a.dst[i];
+      q[1] = a.phase ? a.size[i] + 1ull : 0ull;
+      q[2] = a.phase ? a.depth[i] + 1ull : 0ull;
+      if (a.phase) a.alive[i] = 0;
+    }
+  }
+}
+
+// Phase 0: count in-degrees.  Phase 1: fold, and collect the records whose in-degree
+// reaches zero into the next frontier.
+__global__ void apply_kernel(int phase, const uint64_t* __restrict__ msgs, uint64_t m,
+                             const uint64_t* __restrict__ src, uint64_t n, unsigned int* indeg,
+                             unsigned long long* size, unsigned long long* depth, uint64_t* __restrict__ fnext,
+                             unsigned long long* cnt_next, unsigned int* err) {
+  WARP_STRIDE(k0, m) {
+    const uint64_t k = k0 + (threadIdx.x & 31u);
+    bool push = false;
+    uint64_t j = kNone;
+    if (k < m) {
+      j = find_source(src, n, msgs[3 * k]);
+      if (phase == 0) {
+        if (j != kNone) atomicAdd(&indeg[j], 1u);
+      } else if (j == kNone) {
+        atomicExch(err, 2u);
+      } else {
+        atomicAdd(&size[j], static_cast<unsigned long long>(msgs[3 * k + 1]));
+        atomicMax(&depth[j], static_cast<unsigned long long>(msgs[3 * k + 2]));
+        push = atomicSub(&indeg[j], 1u) == 1u;
+      }
+    }
+    if (phase) warp_append(push, j, fnext, cnt_next);
+  }
 }
 
 // ------------------------------------------------------------------ cycles (step 5)
@@ -377,72 +424,80 @@ struct ReduceScratch {
 };
 
 size_t reduce_scratch_bytes(uint64_t n, uint32_t max_stats) {
-  // stamp (u32), newpos, idx x2, second set of five columns, tile counts, control, stats
+  // err, control, pass stats, tile counts, idx, in-degree, alive flags, two frontiers
   const uint64_t tiles = (n + kTile - 1) / kTile + 1;
-  return n * 4 + 8 * n * 8 + tiles * 8 + 3ull * (max_stats + 1) * 8 + 64 * 1024 + 16 * 256;
+  return 16 * 256 + tiles * 8 + 3ull * (max_stats + 1) * 8 + n * (8 + 4 + 1 + 8 + 8) + 8 * 256;
 }
 
 namespace {
 
-struct PassLaunch {
-  unsigned grid, tgrid;
-  PassCtl* ctl;
-  uint32_t* stamp;
-  uint64_t* tiles;
-  uint64_t* newpos;
-  uint64_t* pstats;
-  uint64_t max_stats;
-  unsigned int* err;
-};
+constexpr int kFoldGrid = 148 * 8;
 
-void launch_pass(const PassLaunch& L, const Cols& c, const Cols& o, cudaStream_t st) {
-  pass_begin_kernel<<<1, 1, 0, st>>>(L.ctl);
-  mark_stamp_kernel<<<L.grid, kT, 0, st>>>(c.idx, L.ctl, L.stamp);
-  fold_stamp_kernel<<<L.grid, kT, 0, st>>>(c.idx, L.ctl, L.stamp, reinterpret_cast<unsigned long long*>(c.size),
-                                           reinterpret_cast<unsigned long long*>(c.depth), L.err);
-  tile_count_stamp_kernel<<<L.tgrid, kT, 0, st>>>(L.stamp, L.ctl, L.tiles);
-  tile_scan_dev_kernel<<<1, 1024, 0, st>>>(L.tiles, L.ctl);
-  rank_stamp_kernel<<<L.tgrid, kT, 0, st>>>(L.stamp, L.ctl, L.tiles, L.newpos);
-  scatter_dev_kernel<<<L.grid, kT, 0, st>>>(c, o, L.newpos, L.ctl);
-  sum_dev_kernel<<<L.grid, kT, 0, st>>>(o.size, L.ctl, L.tiles);
-  pass_end_kernel<<<1, 1, 0, st>>>(L.ctl, L.tiles, L.pstats, L.max_stats);
+// Stable compaction of the five record columns to the rows with flag != 0 (in place, via
+// tmp); returns the surviving count on the host.
+cudaError_t compact_records(uint64_t n, const uint8_t* flag, uint64_t* const cols[5], uint64_t* tiles_buf,
+                            uint64_t* newpos, uint64_t* tmp, uint64_t* n_out, cudaStream_t st, int* launches) {
+  const uint64_t tiles = (n + kTile - 1) / kTile;
+  tile_count_kernel<<<static_cast<unsigned>(tiles), kT, 0, st>>>(flag, n, tiles_buf);
+  tile_scan_kernel<<<1, 1024, 0, st>>>(tiles_buf, tiles);
+  rank_kernel<<<static_cast<unsigned>(tiles), kT, 0, st>>>(flag, n, tiles_buf, newpos);
+  *launches += 3;
+  cudaError_t e;
+  uint64_t m = 0;
+  if ((e = cudaMemcpyAsync(&m, &tiles_buf[tiles], 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  if (m != n) {
+    for (int k = 0; k < 5; ++k) {
+      select_kernel<<<grid_for(n), kT, 0, st>>>(newpos, n, cols[k], tmp);
+      ++*launches;
+      if (m && (e = cudaMemcpyAsync(cols[k], tmp, m * 8, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
+    }
+  }
+  *n_out = m;
+  return cudaGetLastError();
 }
-
-constexpr int kLaunchesPerPass = 9;
 
 }  // namespace
 
-// Passes run back to back on the device: every kernel reads the current record count
-// and pass number from PassCtl, so the host only checks in every 32 passes (a CUDA graph
-// of two ping-pong passes replayed 16 times).  Passes after the fixpoint are no-ops
-// (nothing removed, every record kept), so overshooting is harmless.
+// Single-GPU leaf cutting: resolve destinations once, count in-degrees, then run passes
+// of two kernels each (fold the frontier; close the pass).  max_passes > 0 launches that
+// many passes directly; 0 runs to the fixpoint from a CUDA graph of two ping-pong passes,
+// checking in with the host after 8, 16, 32 ... graph replays.  Passes after the fixpoint
+// are no-ops, so overshooting is harmless.
 cudaError_t cut_leaves_device(uint64_t n, uint64_t* src, uint64_t* dst, uint64_t* dist, uint64_t* size,
                               uint64_t* depth, uint32_t max_passes, uint64_t* pass_stats, uint32_t max_stats,
                               uint32_t* n_passes, uint64_t* n_out, unsigned int* err_out, void* scratch,
                               cudaStream_t st, int* launches) {
   ReduceScratch s{static_cast<uint8_t*>(scratch), 0};
   unsigned int* err = s.take<unsigned int>(4);
-  PassCtl* ctl = s.take<PassCtl>(1);
+  CutCtl* ctl = s.take<CutCtl>(1);
   const uint64_t stats_cap = max_stats ? max_stats : 1;
   uint64_t* pstats = s.take<uint64_t>(3 * stats_cap);
   uint64_t* tiles_buf = s.take<uint64_t>((n + kTile - 1) / kTile + 1);
-  uint32_t* stamp = s.take<uint32_t>(n);
-  uint64_t* newpos = s.take<uint64_t>(n);
-  Cols a{src, dst, dist, size, depth, s.take<uint64_t>(n)};
-  Cols b{s.take<uint64_t>(n), s.take<uint64_t>(n), s.take<uint64_t>(n), s.take<uint64_t>(n), s.take<uint64_t>(n),
-         s.take<uint64_t>(n)};
+  uint64_t* idx = s.take<uint64_t>(n);
+  unsigned int* indeg = s.take<unsigned int>(n);
+  uint8_t* alive = s.take<uint8_t>(n);
+  uint64_t* f0 = s.take<uint64_t>(n);
+  uint64_t* f1 = s.take<uint64_t>(n);
   cudaError_t e;
   *n_passes = 0;
   *n_out = n;
   *err_out = 0;
   if (n == 0) return cudaSuccess;
+  auto* usize = reinterpret_cast<unsigned long long*>(size);
+  auto* udepth = reinterpret_cast<unsigned long long*>(depth);
   if ((e = cudaMemsetAsync(err, 0, 16, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(ctl, 0, sizeof(CutCtl), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(indeg, 0, n * sizeof(unsigned int), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(alive, 1, n, st)) != cudaSuccess) return e;
   check_sorted_kernel<<<grid_for(n), kT, 0, st>>>(src, n, err);
-  resolve_kernel<<<grid_for(n), kT, 0, st>>>(src, n, dst, a.idx);
-  *launches += 2;
-  if ((e = cudaMemsetAsync(stamp, 0, n * sizeof(uint32_t), st)) != cudaSuccess) return e;
-  const PassCtl init{n, 0, 0, 0, 0};
-  if ((e = cudaMemcpyAsync(ctl, &init, sizeof(init), cudaMemcpyHostToDevice, st)) != cudaSuccess) return e;
+  resolve_kernel<<<grid_for(n), kT, 0, st>>>(src, n, dst, idx);
+  indeg_count_kernel<<<grid_for(n), kT, 0, st>>>(idx, n, indeg);
+  frontier_init_kernel<<<grid_for(n), kT, 0, st>>>(indeg, n, f0, &ctl->cnt[0]);
+  sum_kernel<<<std::min(grid_for(n), 4096u), kT, 0, st>>>(size, n, &ctl->sum);
+  *launches += 5;
+  const unsigned long long alive0 = n;
+  if ((e = cudaMemcpyAsync(&ctl->alive, &alive0, 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) return e;
   unsigned int herr = 0;
   if ((e = cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
@@ -450,16 +505,17 @@ cudaError_t cut_leaves_device(uint64_t n, uint64_t* src, uint64_t* dst, uint64_t
     *err_out = herr;
     return cudaSuccess;
   }
-  const uint64_t tiles0 = (n + kTile - 1) / kTile;
-  PassLaunch L{std::min(grid_for(n), 4096u), static_cast<unsigned>(std::min<uint64_t>(tiles0, 4096)), ctl, stamp,
-               tiles_buf, newpos, pstats, max_stats, err};
-  PassCtl h{};
+  auto pass = [&](int w) {
+    cut_fold_kernel<<<kFoldGrid, kT, 0, st>>>(ctl, w, w ? f1 : f0, w ? f0 : f1, idx, usize, udepth, indeg, alive,
+                                              err);
+    cut_pass_end_kernel<<<1, 1, 0, st>>>(ctl, w, pstats, max_stats);
+  };
+  constexpr int kLaunchesPerPass = 2;
+  CutCtl h{};
   uint64_t executed = 0;
   if (max_passes != 0) {
-    for (uint32_t k = 0; k < max_passes; ++k) {
-      launch_pass(L, (k & 1) ? b : a, (k & 1) ? a : b, st);
-      *launches += kLaunchesPerPass;
-    }
+    for (uint32_t k = 0; k < max_passes; ++k) pass(static_cast<int>(k & 1));
+    *launches += kLaunchesPerPass * max_passes;
     executed = max_passes;
     if ((e = cudaMemcpyAsync(&h, ctl, sizeof(h), cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
     if ((e = cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
@@ -468,17 +524,16 @@ cudaError_t cut_leaves_device(uint64_t n, uint64_t* src, uint64_t* dst, uint64_t
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     if ((e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) return e;
-    launch_pass(L, a, b, st);
-    launch_pass(L, b, a, st);
+    pass(0);
+    pass(1);
     if ((e = cudaStreamEndCapture(st, &graph)) != cudaSuccess) return e;
     if ((e = cudaGraphInstantiate(&exec, graph, 0)) != cudaSuccess) return e;
-    constexpr int kBatch = 16;  // graphs (x2 passes) per host check-in
-    for (;;) {
-      for (int k = 0; k < kBatch; ++k)
+    for (int batch = 8;; batch = std::min(batch * 2, 512)) {  // graphs (x2 passes) per host check-in
+      for (int k = 0; k < batch; ++k)
         if ((e = cudaGraphLaunch(exec, st)) != cudaSuccess) break;
       if (e != cudaSuccess) break;
-      executed += 2 * kBatch;
-      *launches += 2 * kBatch * kLaunchesPerPass;
+      executed += 2 * batch;
+      *launches += 2 * batch * kLaunchesPerPass;
       if ((e = cudaMemcpyAsync(&h, ctl, sizeof(h), cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
       if ((e = cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
       if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
@@ -498,15 +553,141 @@ cudaError_t cut_leaves_device(uint64_t n, uint64_t* src, uint64_t* dst, uint64_t
   if (keep_stats)
     if ((e = cudaMemcpyAsync(pass_stats, pstats, keep_stats * 3 * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
       return e;
-  // an odd number of executed passes leaves the survivors in the second column set
-  if (executed & 1) {
-    for (int k = 0; k < 5; ++k)
-      if ((e = cudaMemcpyAsync((&a.src)[k], (&b.src)[k], h.n * 8, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
-        return e;
+  uint64_t* cols[5] = {src, dst, dist, size, depth};
+  return compact_records(n, alive, cols, tiles_buf, f0, f1, n_out, st, launches);
+}
+
+// ---- sharded leaf cutting: per-rank state and the three host-called steps.
+
+size_t shard_scratch_bytes(uint64_t n, uint32_t n_ranks) {
+  const uint64_t tiles = (n + kTile - 1) / kTile + 1;
+  return 16 * 256 + tiles * 8 + 4ull * n_ranks * 8 + 2 * 256 + n * (4 + 1 + 8 + 8) + 8 * 256;
+}
+
+cudaError_t shard_init(ShardState* sh, void* scratch, uint64_t n, uint64_t* const cols[5], uint32_t n_ranks,
+                       const uint64_t* rank_first, const uint64_t* rank_count, uint64_t* size_sum,
+                       unsigned int* err_out, cudaStream_t st, int* launches) {
+  ReduceScratch s{static_cast<uint8_t*>(scratch), 0};
+  sh->n = n;
+  for (int k = 0; k < 5; ++k) sh->cols[k] = cols[k];
+  sh->n_ranks = n_ranks;
+  sh->err = s.take<unsigned int>(4);
+  sh->ctl = s.take<CutCtl>(1);
+  sh->tiles = s.take<uint64_t>((n + kTile - 1) / kTile + 1);
+  sh->bounds = s.take<uint64_t>(n_ranks);
+  sh->brank = s.take<uint32_t>(n_ranks);
+  sh->ocount = s.take<unsigned long long>(n_ranks);
+  sh->ocursor = s.take<unsigned long long>(n_ranks);
+  sh->indeg = s.take<unsigned int>(n);
+  sh->alive = s.take<uint8_t>(n);
+  sh->f[0] = s.take<uint64_t>(n);
+  sh->f[1] = s.take<uint64_t>(n);
+  sh->w = 0;
+  sh->started = false;
+  // owner table over the non-empty ranks; the first bound is 0 so every value has an owner
+  uint64_t hb[kMaxShardRanks];
+  uint32_t hr[kMaxShardRanks];
+  uint32_t nb = 0;
+  for (uint32_t r = 0; r < n_ranks; ++r) {
+    if (rank_count[r] == 0) continue;
+    hb[nb] = nb == 0 ? 0 : rank_first[r];
+    hr[nb] = r;
+    ++nb;
   }
+  if (nb == 0) {  // every shard empty: a single owner so the tables stay well-formed
+    hb[0] = 0;
+    hr[0] = 0;
+    nb = 1;
+  }
+  sh->nb = nb;
+  cudaError_t e;
+  *err_out = 0;
+  *size_sum = 0;
+  if ((e = cudaMemcpyAsync(sh->bounds, hb, nb * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) return e;
+  if ((e = cudaMemcpyAsync(sh->brank, hr, nb * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(sh->err, 0, 16, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(sh->ctl, 0, sizeof(CutCtl), st)) != cudaSuccess) return e;
+  if (n) {
+    if ((e = cudaMemsetAsync(sh->indeg, 0, n * 4, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(sh->alive, 1, n, st)) != cudaSuccess) return e;
+    check_sorted_kernel<<<grid_for(n), kT, 0, st>>>(cols[0], n, sh->err);
+    sum_kernel<<<std::min(grid_for(n), 4096u), kT, 0, st>>>(cols[3], n, &sh->ctl->sum);
+    *launches += 2;
+  }
+  unsigned long long hs = 0;
+  if ((e = cudaMemcpyAsync(&hs, &sh->ctl->sum, 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+  if ((e = cudaMemcpyAsync(err_out, sh->err, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
-  *n_out = h.n;
-  return cudaSuccess;
+  *size_sum = hs;
+  return cudaGetLastError();
+}
+
+cudaError_t shard_emit(ShardState* sh, int phase, uint64_t* send, uint64_t* counts, uint64_t* info,
+                       cudaStream_t st, int* launches) {
+  cudaError_t e;
+  if (phase && !sh->started) {  // all in-degree messages have been applied: first frontier
+    if (sh->n) {
+      frontier_init_kernel<<<grid_for(sh->n), kT, 0, st>>>(sh->indeg, sh->n, sh->f[0], &sh->ctl->cnt[0]);
+      ++*launches;
+    }
+    sh->started = true;
+  }
+  if ((e = cudaMemsetAsync(sh->ocount, 0, sh->n_ranks * 8ull, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(sh->ocursor, 0, sh->n_ranks * 8ull, st)) != cudaSuccess) return e;
+  if (phase && (e = cudaMemsetAsync(&sh->ctl->cnt[sh->w ^ 1], 0, 8, st)) != cudaSuccess) return e;
+  EmitArgs a{phase,
+             sh->n,
+             sh->ctl,
+             sh->w,
+             sh->f[sh->w],
+             sh->cols[1],
+             reinterpret_cast<const unsigned long long*>(sh->cols[3]),
+             reinterpret_cast<const unsigned long long*>(sh->cols[4]),
+             sh->alive,
+             sh->bounds,
+             sh->brank,
+             sh->nb,
+             sh->n_ranks,
+             sh->ocount,
+             sh->ocursor,
+             send};
+  const unsigned g = phase ? static_cast<unsigned>(kFoldGrid) : std::min(grid_for(sh->n), 4096u);
+  emit_count_kernel<<<g, kT, 0, st>>>(a);
+  emit_write_kernel<<<g, kT, 0, st>>>(a);
+  *launches += 2;
+  unsigned long long items = 0;
+  unsigned int herr = 0;
+  if ((e = cudaMemcpyAsync(counts, sh->ocount, sh->n_ranks * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+  if (phase && (e = cudaMemcpyAsync(&items, &sh->ctl->cnt[sh->w], 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    return e;
+  if ((e = cudaMemcpyAsync(&herr, sh->err, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  info[0] = phase ? items : sh->n;
+  info[1] = herr;
+  return cudaGetLastError();
+}
+
+cudaError_t shard_apply(ShardState* sh, int phase, const uint64_t* msgs, uint64_t m, cudaStream_t st,
+                        int* launches) {
+  if (m) {
+    const unsigned g = std::min(grid_for(m), phase ? static_cast<unsigned>(kFoldGrid) : 4096u);
+    apply_kernel<<<g, kT, 0, st>>>(phase, msgs, m, sh->cols[0], sh->n, sh->indeg,
+                                   reinterpret_cast<unsigned long long*>(sh->cols[3]),
+                                   reinterpret_cast<unsigned long long*>(sh->cols[4]), sh->f[sh->w ^ 1],
+                                   &sh->ctl->cnt[sh->w ^ 1], sh->err);
+    ++*launches;
+  }
+  if (phase) sh->w ^= 1;  // the frontier just filled is the next pass's
+  return cudaGetLastError();
+}
+
+cudaError_t shard_finish(ShardState* sh, uint64_t* n_out, unsigned int* err_out, cudaStream_t st, int* launches) {
+  cudaError_t e;
+  *n_out = sh->n;
+  if ((e = cudaMemcpyAsync(err_out, sh->err, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  if (*err_out || sh->n == 0) return cudaSuccess;
+  return compact_records(sh->n, sh->alive, sh->cols, sh->tiles, sh->f[0], sh->f[1], n_out, st, launches);
 }
 
 size_t cycles_scratch_bytes(uint64_t n) { return 10 * n * 8 + n + ((n + kTile - 1) / kTile + 1) * 8 + 8192; }

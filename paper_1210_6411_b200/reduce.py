@@ -33,7 +33,7 @@ from .records import EDGE_SIZE, EdgeRecord, read_edge_arrays, write_edge_arrays
 
 __all__ = ["ReduceConfig", "PassStats", "IterationLog", "CycleRecord", "cut_leaves_pass",
            "cut_leaves_to_fixpoint", "count_cycles", "NotAPermutationError", "sort_edge_arrays",
-           "cut_leaves_arrays", "count_cycles_arrays"]
+           "cut_leaves_arrays", "cut_leaves_tensors", "count_cycles_arrays"]
 
 _MIN_BUDGET = 3 * (1 << 20)
 
@@ -140,6 +140,33 @@ def cut_leaves_arrays(src, dst, dist, subtree_size, subtree_depth, *, max_passes
     m = int(nout.value)
     passes = [tuple(int(v) for v in stats[i]) for i in range(min(int(npass.value), cap))]
     return tuple(c[:m] for c in cols) + (passes,)
+
+
+def cut_leaves_tensors(src, dst, dist, subtree_size, subtree_depth, *, max_passes: int = 0):
+    """Leaf cutting on device-resident torch columns (64-bit, contiguous, one CUDA device,
+    sorted by unique source), in place on the current stream.  Returns (n_out, passes):
+    the first n_out rows are the survivors."""
+    import torch
+
+    cols = (src, dst, dist, subtree_size, subtree_depth)
+    dev = src.device
+    for c in cols:
+        if c.device != dev or c.device.type != "cuda" or c.element_size() != 8 or not c.is_contiguous():
+            raise ValueError("columns must be contiguous 64-bit tensors on one CUDA device")
+        if c.numel() != src.numel():
+            raise ValueError("columns differ in length")
+    cap = 1 << 16
+    stats = np.zeros((cap, 3), dtype=np.uint64)
+    npass = C.c_uint32(0)
+    nout = C.c_uint64(0)
+    ctx = N.context(dev.index)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    rc = N.lib.lc_cut_leaves_device(ctx.handle, src.numel(), *(c.data_ptr() for c in cols), int(max_passes),
+                                    N.u64p(stats), cap, C.byref(npass), C.byref(nout), stream)
+    if rc != N.LC_OK:
+        _raise(rc)
+    passes = [tuple(int(v) for v in stats[i]) for i in range(min(int(npass.value), cap))]
+    return int(nout.value), passes
 
 
 def count_cycles_arrays(src, dst, dist, subtree_size):
