@@ -319,18 +319,63 @@ __device__ __forceinline__ Node<S> expand_node(uint64_t y, uint32_t F) {
   return nd;
 }
 
-// One traversal step of a candidate's segment.  State: x (current node), d (depth),
-// acc (expanded for dfs / node count for bfs), pop (x is about to be expanded; else we
-// are backtracking from x).  Returns 0 while running, 1 = finished shallow, 2 = finished
-// deep (not shallow).
+// Child q of the node y (its registers unstepped on demand): used when resuming a
+// pending branch point.
 template <class S>
-__device__ __forceinline__ int prune_step(uint64_t& x, uint64_t& d, uint64_t& acc, bool& pop, uint32_t F,
-                                          int mode, uint64_t limit) {
-  if (!pop && d == 0) return 1;  // back at the root: traversal complete
-  const uint64_t y = pop ? x : clock_scalar<S>(x);
+__device__ __forceinline__ uint64_t child_of(uint64_t y, int q) {
+  const uint32_t r1 = static_cast<uint32_t>(y & S::M1), r2 = static_cast<uint32_t>((y >> S::O2) & S::M2),
+                 r3 = static_cast<uint32_t>((y >> S::O3) & S::M3);
+  const int p = clock_pattern(q & 3);
+  const uint32_t p1 = (p & 1) ? unstep<S::L1, S::T1>(r1) : r1, p2 = (p & 2) ? unstep<S::L2, S::T2>(r2) : r2,
+                 p3 = (p & 4) ? unstep<S::L3, S::T3>(r3) : r3;
+  return static_cast<uint64_t>(p1) | (static_cast<uint64_t>(p2) << S::O2) | (static_cast<uint64_t>(p3) << S::O3);
+}
+
+// Pending branch points of a lane's traversal: a ring of the kRing deepest nodes that
+// still have unvisited (lower) children, in shared memory ([slot][thread], conflict-free).
+// Backtracking pops the deepest one and jumps straight to its next child instead of
+// climbing the path one forward clock (and one re-expansion) per level.  If the ring
+// overflowed, the oldest entries are gone; once it runs empty the traversal falls back to
+// the stackless climb, which rediscovers them (and an empty ring without overflow means
+// the traversal is complete -- no climb back to the root).
+constexpr int kRing = 8;
+
+struct Ring {
+  uint32_t* lo;  // [kRing][kThreads]: node low word
+  uint32_t* hi;  //                   node high word
+  uint32_t* dm;  //                   depth << 4 | remaining child mask
+  uint32_t top, cnt;
+  bool lost;
+  __device__ __forceinline__ uint32_t at(uint32_t slot) const { return slot * kThreads + threadIdx.x; }
+  __device__ __forceinline__ void push(uint64_t y, uint64_t d, uint32_t mask) {
+    if (d >= (1ull << 27)) {  // depth does not fit the slot: leave it to the stackless climb
+      lost = true;
+      return;
+    }
+    top = (top + 1) & (kRing - 1);
+    lo[at(top)] = static_cast<uint32_t>(y);
+    hi[at(top)] = static_cast<uint32_t>(y >> 32);
+    dm[at(top)] = (static_cast<uint32_t>(d) << 4) | mask;
+    if (cnt == kRing) lost = true;
+    else ++cnt;
+  }
+};
+
+// One traversal step of a candidate's segment: exactly one node expansion per step for
+// every lane (uniform across the warp).  State: x (the node to expand next), d (its
+// depth), acc (expanded for dfs / node count for bfs), climb (x's subtree is finished and
+// the ring lost entries: this step expands x's parent to find x's next-lower sibling).
+// Returns 0 while running, 1 = finished shallow, 2 = finished deep (not shallow).
+template <class S>
+__device__ __forceinline__ int prune_step(uint64_t& x, uint64_t& d, uint64_t& acc, bool& climb, Ring& ring,
+                                          uint32_t F, int mode, uint64_t limit) {
+  uint64_t y = x;
+  if (climb) y = clock_scalar<S>(x);  // x's parent
   const Node<S> nd = expand_node<S>(y, F);
-  if (pop) {
-    if (nd.mask != 0u) {
+  bool leaf;
+  if (!climb) {
+    leaf = nd.mask == 0u;
+    if (!leaf) {
       if (mode == 0) {
         if (d >= limit) {  // a child would sit below the depth limit
           acc += 1;
@@ -344,26 +389,54 @@ __device__ __forceinline__ int prune_step(uint64_t& x, uint64_t& d, uint64_t& ac
           return 2;
         }
       }
-      x = nd.child(31 - __clz(nd.mask));  // the reference pops the last child first
+      const int q = 31 - __clz(nd.mask);  // the reference pops the last child first
+      const uint32_t rest = nd.mask & ~(1u << q);
+      if (rest) ring.push(x, d, rest);
+      x = nd.child(q);
       ++d;
-    } else {
-      pop = false;
+      return 0;
     }
   } else {
-    // y is x's parent; continue with x's next-lower sibling, else climb
+    // continue with x's next-lower sibling, else keep climbing
     uint32_t q = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k)
       if (((nd.mask >> k) & 1u) && nd.child(k) == x) q = k;
     const uint32_t lower = nd.mask & ((1u << q) - 1u);
     if (lower != 0u) {
-      x = nd.child(31 - __clz(lower));
-      pop = true;
-    } else {
-      x = y;
-      --d;
+      const int c = 31 - __clz(lower);
+      const uint32_t rest = lower & ~(1u << c);
+      if (rest) ring.push(y, d - 1, rest);
+      x = nd.child(c);
+      climb = false;
+      return 0;
     }
+    x = y;
+    --d;
+    leaf = true;  // y's subtree is finished too
   }
+  // x's subtree is finished: resume the deepest pending branch point
+  if (ring.cnt) {
+    const uint32_t slot = ring.at(ring.top);
+    const uint64_t p = static_cast<uint64_t>(ring.lo[slot]) | (static_cast<uint64_t>(ring.hi[slot]) << 32);
+    const uint32_t dm = ring.dm[slot];
+    const uint32_t mask = dm & 15u;
+    const int q = 31 - __clz(mask);
+    const uint32_t rest = mask & ~(1u << q);
+    if (rest) {
+      ring.dm[slot] = (dm & ~15u) | rest;
+    } else {
+      ring.top = (ring.top - 1) & (kRing - 1);
+      --ring.cnt;
+    }
+    x = child_of<S>(p, q);
+    d = (dm >> 4) + 1;
+    climb = false;
+    return 0;
+  }
+  if (!ring.lost || d == 0) return 1;  // nothing pending: traversal complete
+  climb = true;
+  (void)leaf;
   return 0;
 }
 
@@ -376,9 +449,11 @@ __global__ void __launch_bounds__(kThreads) prune_kernel(const uint64_t* __restr
                                                          uint8_t* __restrict__ removed,
                                                          uint64_t* __restrict__ work,
                                                          unsigned long long* queue) {
+  __shared__ uint32_t ring_lo[kRing * kThreads], ring_hi[kRing * kThreads], ring_dm[kRing * kThreads];
   const uint32_t lane = threadIdx.x & 31u;
   uint64_t i = 0, x = 0, d = 0, acc = 0;
-  bool have = false, pop = true, drained = false;
+  bool have = false, climb = false, drained = false;
+  Ring ring{ring_lo, ring_hi, ring_dm, 0, 0, false};
   for (;;) {
     if (!drained) {
       const uint32_t need = __ballot_sync(kFull, !have);
@@ -394,15 +469,17 @@ __global__ void __launch_bounds__(kThreads) prune_kernel(const uint64_t* __restr
             x = cands[i];
             d = 0;
             acc = mode == 0 ? 0 : 1;
-            pop = true;
+            climb = false;
             have = true;
+            ring.cnt = 0;
+            ring.lost = false;
           }
         }
       }
     }
     if (!__any_sync(kFull, have)) break;
     if (have) {
-      const int r = prune_step<S>(x, d, acc, pop, F, mode, limit);
+      const int r = prune_step<S>(x, d, acc, climb, ring, F, mode, limit);
       if (r != 0) {
         removed[i] = r == 1 ? 1 : 0;
         work[i] = acc;
