@@ -291,6 +291,30 @@ struct Node {
   }
 };
 
+// The predecessor table as 64 nibbles (bit q of nibble idx = pattern q consistent at
+// table index idx), packed in four 64-bit immediates.
+constexpr uint64_t nibble_word_ce(int w) {
+  uint64_t v = 0;
+  for (int k = 0; k < 16; ++k)
+    for (int q = 0; q < 4; ++q)
+      if ((pattern_mask(q) >> (16 * w + k)) & 1ull) v |= 1ull << (4 * k + q);
+  return v;
+}
+constexpr uint64_t kNib0 = nibble_word_ce(0), kNib1 = nibble_word_ce(1), kNib2 = nibble_word_ce(2),
+                   kNib3 = nibble_word_ce(3);
+
+__device__ __forceinline__ uint32_t pattern_set(uint32_t idx) {
+  const uint64_t w = idx < 32 ? (idx < 16 ? kNib0 : kNib1) : (idx < 48 ? kNib2 : kNib3);
+  return static_cast<uint32_t>(w >> ((idx & 15u) << 2)) & 15u;
+}
+
+// Children of y in the segment: y's predecessors (cipher.py:342-369) minus special
+// nodes (pipeline.py:121-129).  Two facts keep this short: predecessors of a valid state
+// never have a zero register (unstep is a bijection fixing 0), and a child c's successor
+// is y itself, so is_candidate(c) (cipher.py:420-428) = R3(c) == F && R3(y) != F &&
+// preds(c) != {} -- only patterns that unstep R3 can land on the plane, and only when
+// unstep(R3(y)) == F (then R3(y) != F automatically); that rare case pays for the
+// children's table lookups.
 template <class S>
 __device__ __forceinline__ Node<S> expand_node(uint64_t y, uint32_t F) {
   Node<S> nd;
@@ -300,20 +324,11 @@ __device__ __forceinline__ Node<S> expand_node(uint64_t y, uint32_t F) {
   nd.u1 = unstep<S::L1, S::T1>(nd.r1);
   nd.u2 = unstep<S::L2, S::T2>(nd.r2);
   nd.u3 = unstep<S::L3, S::T3>(nd.r3);
-  const uint32_t idx = table_index<S>(y);
-  uint32_t m = 0;
+  uint32_t m = pattern_set(table_index<S>(y));
+  if (nd.u3 == F) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    if ((pattern_mask(q) >> idx) & 1ull) {
-      const int p = clock_pattern(q);
-      const uint32_t p1 = (p & 1) ? nd.u1 : nd.r1, p2 = (p & 2) ? nd.u2 : nd.r2,
-                     p3 = (p & 4) ? nd.u3 : nd.r3;
-      if (p1 != 0u && p2 != 0u && p3 != 0u) {
-        bool cand = false;
-        if (p3 == F) cand = is_candidate<S>(nd.child(q), F);
-        if (!cand) m |= 1u << q;
-      }
-    }
+    for (int q = 1; q < 4; ++q)
+      if (((m >> q) & 1u) && ((kNonEmpty >> table_index<S>(nd.child(q))) & 1ull)) m &= ~(1u << q);
   }
   nd.mask = m;
   return nd;
