@@ -271,10 +271,11 @@ def main() -> None:
     e2e = None
     if not args.no_e2e:
         hp = [C.c_void_p() for _ in range(4)]
-        for p, nbytes in zip(hp, (batch * 8, batch * 8, batch * 8, words * 8)):
-            N.check(N.lib.lc_host_alloc(nbytes, C.byref(p)))
+        sizes = (batch, batch * LEGS, batch * LEGS, words)
+        for p, n in zip(hp, sizes):
+            N.check(N.lib.lc_host_alloc(n * 8, C.byref(p)))
         h_starts, h_dst, h_dist, h_stats = (np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_uint64)), shape=(n,))
-                                            for p, n in zip(hp, (batch, batch, batch, words)))
+                                            for p, n in zip(hp, sizes))
         e2e_tr = 0
         e2e_el = 0.0
         if world > 1:
@@ -283,8 +284,8 @@ def main() -> None:
             b = k % nbatches
             h_starts[:] = starts[b * batch:(b + 1) * batch].cpu().numpy().view(np.uint64)
             t0 = time.perf_counter()
-            N.check(N.lib.lc_walk(ctx.handle, C.byref(sspec), params.fixed_r3, N.u64p(h_starts), batch, STRIDE,
-                                  CAP, 1, args.refill, N.u64p(h_dst), N.u64p(h_dist), hist_lo,
+            N.check(N.lib.lc_walk(ctx.handle, C.byref(sspec), params.fixed_r3, N.u64p(h_starts), batch, STRIDE_,
+                                  CAP, LEGS, args.refill, N.u64p(h_dst), N.u64p(h_dist), hist_lo,
                                   hist_shift, hist_bins, N.u64p(h_stats)))
             e2e_el += time.perf_counter() - t0
             e2e_tr += int(h_stats[N.ST_TRANSITIONS])
@@ -296,7 +297,7 @@ def main() -> None:
             dist.all_reduce(tt)
             e2e_tr = int(tt.item())
         e2e = {"value": e2e_tr / e2e_el, "unit": "transitions/s", "h2d_bytes_per_step": batch * 8,
-               "d2h_bytes_per_step": batch * 16 + words * 8,
+               "d2h_bytes_per_step": batch * LEGS * 16 + words * 8,
                "note": "lc_walk host-buffer C ABI call from pinned memory, wall clock"}
         for p in hp:
             N.lib.lc_host_free(p)
