@@ -2,9 +2,10 @@
 the leaf/predecessor filter over a 2^32-state slice of the fixed-R3 plane (K2), the
 step-2 prune of the resulting candidates (K3), and a walk of the survivors (K1).
 
-    python bench_steps12.py [--rows-log2 13] [--prune-log2 20] [--depth 3000]
+    python bench_steps12.py [--rows-log2 13] [--prune-log2 20] [--depth 3000] [--full]
 
-Prints one JSON line.  Parity: the first 4 R2 rows of the slice and a 2048-candidate
+Prints one JSON line.  --full runs steps 1-3 over the whole slice: every candidate is
+pruned (chunks of 2^26) and every survivor is walked to its next special node.  Parity: the first 4 R2 rows of the slice and a 2048-candidate
 sample of the prune are compared with the C oracle on the host.
 """
 
@@ -31,6 +32,7 @@ def main():
     ap.add_argument("--prune-log2", type=int, default=20)
     ap.add_argument("--depth", type=int, default=3000)     # the paper's DFS depth
     ap.add_argument("--walk-log2", type=int, default=14)
+    ap.add_argument("--full", action="store_true")
     args = ap.parse_args()
 
     import torch
@@ -112,6 +114,10 @@ def main():
     nw = min(1 << args.walk_log2, surv.numel())
     res = lc.walk_arrays(surv[:nw].cpu().numpy().view(np.uint64), params, spec, stride=lc.DEFAULT_STRIDE_A51)
 
+    full = None
+    if args.full:
+        full = full_slice(args, ctx, sspec, params, out[:ncand], stream, torch, N, lc)
+
     line = {
         "metric": "steps 1-2 feeding the walk (special-node enumeration + leaf/predecessor filter, prune)",
         "config": {"workload": f"configs[2]: R3 = 0x2AAA00, R2 in [{R2_0:#x}, {R2_0 + rows:#x}), all R1 "
@@ -128,7 +134,61 @@ def main():
         "k1_walk_survivors": {"walks": nw, "edges": res.edges, "transitions": res.transitions},
         "gpu": torch.cuda.get_device_name(0),
     }
+    if full:
+        line["full_slice_steps_1_to_3"] = full
     print(json.dumps(line), flush=True)
+
+
+def full_slice(args, ctx, sspec, params, cands, stream, torch, N, lc):
+    """Steps 1-3 over the whole slice: prune every candidate (chunks of 2^26 on the
+    device), compact the survivors, walk them all (one lc_walk_device call)."""
+    dev = cands.device
+    n = cands.numel()
+    chunk = 1 << 26
+    removed = torch.empty(chunk, dtype=torch.uint8, device=dev)
+    work = torch.empty(chunk, dtype=torch.int64, device=dev)
+    keep = []
+    expanded = 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for lo in range(0, n, chunk):
+        m = min(chunk, n - lo)
+        N.check(N.lib.lc_prune_device(ctx.handle, C.byref(sspec), params.fixed_r3, 0, args.depth,
+                                      C.c_void_p(cands[lo:].data_ptr()), m, C.c_void_p(removed.data_ptr()),
+                                      C.c_void_p(work.data_ptr()), C.c_void_p(stream.cuda_stream)))
+        keep.append(cands[lo:lo + m][removed[:m] == 0])
+        expanded += int(work[:m].sum().item())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    prune_s = e0.elapsed_time(e1) / 1e3
+    surv = torch.cat(keep)
+    ns = surv.numel()
+    dst = torch.empty(ns, dtype=torch.int64, device=dev)
+    dist = torch.empty(ns, dtype=torch.int64, device=dev)
+    words = N.ST_HEADER + 2
+    st = torch.zeros(words, dtype=torch.int64, device=dev)
+    e0.record(stream)
+    N.check(N.lib.lc_walk_device(ctx.handle, C.byref(sspec), params.fixed_r3, C.c_void_p(surv.data_ptr()), ns,
+                                 lc.DEFAULT_STRIDE_A51, 16 * int(4 * ((1 << 23) - 1) / 3) + 64, 1, 0,
+                                 C.c_void_p(dst.data_ptr()), C.c_void_p(dist.data_ptr()), 0, 0, 0,
+                                 C.c_void_p(st.data_ptr()), C.c_void_p(stream.cuda_stream)))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    walk_s = e0.elapsed_time(e1) / 1e3
+    stats = st.cpu().numpy().view(np.uint64)
+    if int(stats[N.ST_ERROR]):
+        raise SystemExit(f"walk error {int(stats[N.ST_ERROR])}")
+    tr = int(stats[N.ST_TRANSITIONS])
+    # every survivor's destination is a special node (K2/K3's set is closed under the walk
+    # only for the whole plane; here the check is the predicate itself)
+    ok = bool(lc.is_candidate(dst[: 1 << 16].cpu().numpy().view(np.uint64), params, lc.A51).all())
+    return {"candidates": n, "prune_depth": args.depth, "survivors": ns, "survivor_fraction": ns / n,
+            "expanded": expanded, "prune_s": prune_s, "expansions_per_s": expanded / prune_s,
+            "walks": ns, "transitions": tr, "walk_s": walk_s, "transitions_per_s": tr / walk_s,
+            "min_dist": int(stats[N.ST_MIN]), "max_dist": int(stats[N.ST_MAX]),
+            "destinations_are_special_nodes": ok,
+            "steps_1_to_3_s": prune_s + walk_s}
 
 
 if __name__ == "__main__":
