@@ -60,9 +60,20 @@ def main():
                                           C.c_void_p(out.data_ptr()), cap, C.c_void_p(count.data_ptr()),
                                           C.c_void_p(stream.cuda_stream)))
 
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # the write-stream roof of this GPU: a plain fill of the same output bytes
+    n_fill = states // 2
+    out[:n_fill].fill_(1)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(3):
+        out[:n_fill].fill_(1)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    write_peak = n_fill * 8 * 3 / (e0.elapsed_time(e1) / 1e3)
+
     enumerate_slice()  # warm-up
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reps = 3
     e0.record(stream)
     for _ in range(reps):
@@ -125,6 +136,8 @@ def main():
         "k2_enumerate": {"states": states, "candidates": ncand, "seconds": k2_s, "states_per_s": states / k2_s,
                          "candidates_per_s": ncand / k2_s, "bytes_written_per_s": ncand * 8 / k2_s,
                          "hbm_frac_of_copy_peak": ncand * 8 / k2_s / 6546.2e9,
+                         "write_stream_gbs_measured": write_peak / 1e9,
+                         "frac_of_write_stream": ncand * 8 / k2_s / write_peak,
                          "parity_first_4_rows_vs_oracle": k2_parity, "ascending": ascending},
         "k3_prune": {"candidates": npr, "removed": nremoved, "removed_fraction": nremoved / npr,
                      "expanded": expanded, "seconds": k3_s, "candidates_per_s": npr / k3_s,

@@ -235,35 +235,116 @@ __device__ __forceinline__ uint64_t plane_offset(uint64_t r2_lo, uint64_t r2, ui
   return off;
 }
 
+// R1 value of virtual slot v of a row of class a (v counts the R1 = 0 slot when p = 0
+// is allowed): run v >> ct1 is pattern rank (run mod |a|) of high part run / |a|.
+template <class S>
+__device__ __forceinline__ uint32_t slot_r1(uint64_t v, uint32_t a, uint32_t na) {
+  constexpr int CT1 = S::CT1;
+  const uint32_t run = static_cast<uint32_t>(v >> CT1), low = static_cast<uint32_t>(v) & ((1u << CT1) - 1u);
+  const uint32_t high = run / na, rank = run - high * na;
+  uint32_t p = a;
+  if (rank >= 1u) p &= p - 1u;
+  if (rank >= 2u) p &= p - 1u;
+  if (rank >= 3u) p &= p - 1u;
+  return (high << (CT1 + 2)) | (static_cast<uint32_t>(__ffs(p) - 1) << CT1) | low;
+}
+
+// Blocks take equal work units (2^16 virtual slots of one R2 row).  A unit's output range is written as 16-byte
+// aligned pairs of states (plus a single head / tail slot), eight pairs per lane per
+// iteration so each thread keeps eight stores in flight: a warp covers 512 consecutive
+// slots per iteration, which span at most three R1 runs when a run has >= 256 values
+// (A5/1), so the runs' (high part, pattern) cost one warp-uniform division per 512
+// slots and a select per slot.  Minis (short runs) use the per-slot form.
 template <class S>
 __global__ void __launch_bounds__(256) enumerate_plane_kernel(uint64_t r2_lo, uint64_t r2_hi, uint32_t F,
                                                               uint64_t* __restrict__ out, uint64_t cap,
                                                               uint64_t* __restrict__ d_count) {
   constexpr int CT1 = S::CT1;
-  constexpr uint32_t kRun = 1u << CT1;                // consecutive R1 values per run
-  constexpr uint32_t kHigh = 1u << (S::L1 - CT1 - 2); // runs of each pattern per row
+  constexpr uint32_t kLowMask = (1u << CT1) - 1u;
+  constexpr int kU = 8;  // pairs per lane per iteration (a warp covers 512 slots)
+  // work units: a row's virtual slots in equal pieces, so blocks get equal work whatever
+  // the row's pattern count (1..4 runs per 2^(ct1+2) R1 values)
+  constexpr uint64_t kRowSlots = 1ull << S::L1;  // >= any row's virtual slot count
+  constexpr uint64_t kUnitSlots = kRowSlots >= (1ull << 16) ? (1ull << 16) : kRowSlots;
+  constexpr uint64_t kUnitsPerRow = kRowSlots / kUnitSlots;
+  constexpr bool kFast = (1u << CT1) >= 256u;  // then a chunk spans at most 3 runs
   const uint32_t c3 = (F >> S::CT3) & 1u, n3 = (F >> (S::CT3 + 1)) & 1u;
   const uint64_t packed_f = static_cast<uint64_t>(F) << S::O3;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   if (blockIdx.x == 0 && threadIdx.x == 0) *d_count = plane_offset<S>(r2_lo, r2_hi, c3, n3);
-  for (uint64_t r2 = r2_lo + blockIdx.x; r2 < r2_hi; r2 += gridDim.x) {
+  const uint64_t units = (r2_hi - r2_lo) * kUnitsPerRow;
+  for (uint64_t unit = blockIdx.x; unit < units; unit += gridDim.x) {
+    const uint64_t r2 = r2_lo + unit / kUnitsPerRow;
+    const uint64_t u_lo = (unit % kUnitsPerRow) * kUnitSlots;  // this unit's virtual slots
     const uint32_t a = allowed_patterns((r2 >> S::CT2) & 3u, c3, n3);
     const uint32_t na = __popc(a);
-    if (na == 0) continue;
-    const uint64_t base = plane_offset<S>(r2_lo, r2, c3, n3) - (a & 1u);  // slot of (high 0, run 0, low 0)
+    const uint64_t skip = a & 1u;  // virtual slot 0 is R1 = 0 (not a state) when p = 0 is allowed
+    const uint64_t row_end = skip + row_count<S>(a);
+    if (na == 0 || u_lo >= row_end) continue;
+    const uint64_t v_end = min(row_end, u_lo + kUnitSlots);
+    const uint64_t base = plane_offset<S>(r2_lo, r2, c3, n3);  // first output slot of the row
     const uint64_t row_bits = (r2 << S::O2) | packed_f;
-    // warp w takes (high, pattern) runs; lanes walk the run's R1 values
-    for (uint32_t run = warp; run < kHigh * na; run += nwarps) {
-      const uint32_t high = run / na, rank = run - high * na;
-      uint32_t p = a;
-      for (uint32_t k = 0; k < rank; ++k) p &= p - 1u;
-      p = __ffs(p) - 1;
-      const uint32_t r1_base = (high << (CT1 + 2)) | (p << CT1);
-      const uint64_t slot0 = base + static_cast<uint64_t>(run) * kRun;
-      for (uint32_t low = lane; low < kRun; low += 32u) {
-        const uint32_t r1 = r1_base | low;
-        const uint64_t slot = slot0 + low;
-        if (r1 != 0u && slot < cap) out[slot] = row_bits | r1;
+    const uint64_t g0 = base - skip;  // output slot of virtual slot v is g0 + v
+    uint64_t v_first = max(skip, u_lo);
+    if ((g0 + v_first) & 1u) {  // odd start: one single slot
+      if (threadIdx.x == 0 && g0 + v_first < cap) out[g0 + v_first] = row_bits | slot_r1<S>(v_first, a, na);
+      ++v_first;
+    }
+    const uint64_t npairs = (v_end - v_first) >> 1;
+    if ((v_end - v_first) & 1u) {  // single tail slot
+      const uint64_t v = v_end - 1, slot = g0 + v;
+      if (threadIdx.x == 0 && slot < cap) out[slot] = row_bits | slot_r1<S>(v, a, na);
+    }
+    uint32_t prank[4];
+    {
+      uint32_t m = a;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        prank[k] = m ? static_cast<uint32_t>(__ffs(m) - 1) : 0u;
+        m &= m - 1u;
+      }
+    }
+    for (uint64_t it = warp; it * (32 * kU) < npairs; it += nwarps) {
+      const uint64_t vbase = v_first + it * (64 * kU);
+      uint32_t pre[3] = {0, 0, 0}, run0 = 0;
+      if constexpr (kFast) {  // the chunk spans runs run0 .. run0 + 2
+        run0 = static_cast<uint32_t>(vbase >> CT1);
+        uint32_t high = run0 / na, rank = run0 - high * na;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const uint32_t p = rank == 0 ? prank[0] : rank == 1 ? prank[1] : rank == 2 ? prank[2] : prank[3];
+          pre[r] = (high << (CT1 + 2)) | (p << CT1);
+          if (++rank == na) {
+            rank = 0;
+            ++high;
+          }
+        }
+      }
+      ulonglong2 val[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint64_t v = vbase + 64 * u + 2 * lane;
+        uint64_t x0, x1;
+        if constexpr (kFast) {
+          const uint32_t d0 = static_cast<uint32_t>(v >> CT1) - run0, d1 = static_cast<uint32_t>((v + 1) >> CT1) - run0;
+          const uint32_t q0 = d0 == 0 ? pre[0] : d0 == 1 ? pre[1] : pre[2];
+          const uint32_t q1 = d1 == 0 ? pre[0] : d1 == 1 ? pre[1] : pre[2];
+          x0 = row_bits | (q0 | (static_cast<uint32_t>(v) & kLowMask));
+          x1 = row_bits | (q1 | (static_cast<uint32_t>(v + 1) & kLowMask));
+        } else {
+          x0 = row_bits | slot_r1<S>(v, a, na);
+          x1 = row_bits | slot_r1<S>(v + 1, a, na);
+        }
+        val[u] = make_ulonglong2(x0, x1);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint64_t k = it * (32 * kU) + 32 * u + lane;  // pair index
+        const uint64_t slot = g0 + vbase + 64 * u + 2 * lane;  // even
+        if (k < npairs) {
+          if (slot + 1 < cap) *reinterpret_cast<ulonglong2*>(out + slot) = val[u];
+          else if (slot < cap) out[slot] = val[u].x;
+        }
       }
     }
   }
@@ -556,7 +637,8 @@ cudaError_t launch_clock(SpecId id, const uint64_t* xs, uint64_t n, uint64_t t, 
 cudaError_t launch_enumerate(SpecId id, uint32_t F, uint64_t r2_lo, uint64_t r2_hi, uint64_t* out,
                              uint64_t cap, uint64_t* d_count, cudaStream_t stream, int* launches) {
   const uint64_t rows = r2_hi > r2_lo ? r2_hi - r2_lo : 0;
-  const unsigned grid = static_cast<unsigned>(rows == 0 ? 1 : (rows > (1u << 20) ? (1u << 20) : rows));
+  const uint64_t units = rows * 8;  // A5/1: 2^19 virtual slots per row in units of 2^16 (minis: 1 per row)
+  const unsigned grid = static_cast<unsigned>(units == 0 ? 1 : (units > (1u << 20) ? (1u << 20) : units));
   if (launches) *launches += 1;
   LC_DISPATCH(id, enumerate_plane_kernel<S><<<grid, 256, 0, stream>>>(r2_lo, r2_hi, F, out, cap, d_count);
               return cudaGetLastError());
