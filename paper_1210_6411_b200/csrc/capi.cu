@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "lfsr_internal.h"
 
@@ -115,8 +116,10 @@ struct lc_ctx {
   int device = 0;
   int sms = 0;
   cudaStream_t stream = nullptr;
-  DevBuf meta, queue, stats, a, b, c, d, scratch, smmap, pq, pool_a, pool_b;
+  DevBuf meta, queue, stats, a, b, c, d, scratch, smmap, pq, pool_a, pool_b, need3;
   int mapped_sms = -1;  // SMs found by the %smid probe (-1: not probed yet)
+  int need3_id = -1;    // spec / fixed R3 the need3 table was built for
+  uint64_t need3_f = 0;
 };
 
 namespace {
@@ -140,6 +143,33 @@ int ensure_smsp_map(lc_ctx* ctx) {
   LC_CUDA(cudaMemcpyAsync(dmap, map, sizeof(map), cudaMemcpyHostToDevice, ctx->stream));
   LC_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->mapped_sms = k;
+  return LC_OK;
+}
+
+// need3[v] = R3 clocks from R3 value v to the fixed value F (the walk's arming bound):
+// one pass over R3's maximal-period sequence starting at F, built once per (spec, F).
+int ensure_need3(lc_ctx* ctx, lc::SpecId id, uint64_t F) {
+  if (ctx->need3_id == static_cast<int>(id) && ctx->need3_f == F) return LC_OK;
+  int l3;
+  uint32_t taps;
+  switch (id) {
+    case lc::SpecId::A51: l3 = 23; taps = (1u << 7) | (1u << 20) | (1u << 21) | (1u << 22); break;
+    case lc::SpecId::MINI567: l3 = 7; taps = (1u << 5) | (1u << 6); break;
+    case lc::SpecId::MINI789: l3 = 9; taps = (1u << 3) | (1u << 8); break;
+    default: return fail(LC_ERR_UNSUPPORTED, "no R3 table for this spec");
+  }
+  const uint32_t mask = (1u << l3) - 1u, period = mask;
+  std::vector<uint32_t> need(static_cast<size_t>(mask) + 1u, 0u);
+  uint32_t x = static_cast<uint32_t>(F);
+  for (uint32_t k = 0; k < period; ++k) {
+    need[x] = (period - k) % period;
+    x = ((x << 1) & mask) | (static_cast<uint32_t>(__builtin_popcount(x & taps)) & 1u);
+  }
+  if (x != F) return fail(LC_ERR_UNSUPPORTED, "R3 is not a maximal-period register");
+  LC_CUDA(ctx->need3.ensure(need.size() * 4));
+  LC_CUDA(cudaMemcpy(ctx->need3.p, need.data(), need.size() * 4, cudaMemcpyHostToDevice));
+  ctx->need3_id = static_cast<int>(id);
+  ctx->need3_f = F;
   return LC_OK;
 }
 
@@ -181,7 +211,7 @@ int lc_ctx_destroy(lc_ctx* ctx) {
   if (!ctx) return LC_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  for (DevBuf* b : {&ctx->meta, &ctx->queue, &ctx->stats, &ctx->a, &ctx->b, &ctx->c, &ctx->d, &ctx->scratch, &ctx->smmap, &ctx->pq, &ctx->pool_a, &ctx->pool_b})
+  for (DevBuf* b : {&ctx->meta, &ctx->queue, &ctx->stats, &ctx->a, &ctx->b, &ctx->c, &ctx->d, &ctx->scratch, &ctx->smmap, &ctx->pq, &ctx->pool_a, &ctx->pool_b, &ctx->need3})
     b->release();
   cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -236,6 +266,7 @@ int walk_launch(lc_ctx* ctx, const WalkArgs& a, const uint64_t* d_starts, const 
                 unsigned long long* pool_count, uint32_t park_below, cudaStream_t st) {
   int rc = ensure_smsp_map(ctx);
   if (rc) return rc;
+  if ((rc = ensure_need3(ctx, a.id, a.fixed_r3))) return rc;
   const bool static_f = a.fixed_r3 == default_fixed(a.id);
   const int per_sm = lc::walk_blocks_per_sm(a.id, static_f);
   const uint64_t lanes_per_block = lc::kWalkThreads * 32ull;
@@ -292,8 +323,27 @@ int walk_launch(lc_ctx* ctx, const WalkArgs& a, const uint64_t* d_starts, const 
   p.pool = pool;
   p.pool_count = pool_count;
   p.park_below = pool ? park_below : 0u;
-  LC_CUDA(lc::launch_walk(a.id, static_f, p, blocks, st));
-  g_launches += 1;
+  p.need3 = ctx->need3.as<uint32_t>();
+  p.run_if_mode = ~0u;
+  // Re-arming pays for lanes that would otherwise be checked for long stretches: lane
+  // mode (independent lanes), or any walk whose stride is below R3's period.  Whole-warp
+  // walks from special nodes at a stride past the period (the paper's setting) run the
+  // plain variant; in auto mode both variants are launched and the device mode word
+  // picks the one that runs.
+  const bool short_stride = a.stride < (1ull << l3_of(a.id)) - 1;
+  if (short_stride || a.refill == 1u || resume) {
+    LC_CUDA(lc::launch_walk(a.id, static_f, true, p, blocks, st));
+    g_launches += 1;
+  } else if (auto_mode) {
+    p.run_if_mode = 1u;
+    LC_CUDA(lc::launch_walk(a.id, static_f, false, p, blocks, st));
+    p.run_if_mode = 0u;
+    LC_CUDA(lc::launch_walk(a.id, static_f, true, p, blocks, st));
+    g_launches += 2;
+  } else {
+    LC_CUDA(lc::launch_walk(a.id, static_f, a.refill != 1024u, p, blocks, st));  // lane mode re-arms
+    g_launches += 1;
+  }
   return LC_OK;
 }
 

@@ -62,10 +62,15 @@ struct WalkParams {
   unsigned long long* pool_count;
   uint32_t park_below;         // park a drained warp once fewer lanes than this are live
   uint32_t pad2;
+  const uint32_t* need3;       // [2^l3] R3 clocks from each R3 value to fixed_r3 (null: none)
+  uint32_t run_if_mode;        // ~0: always run; else run only if *mode_word equals it
+  uint32_t pad3;
 };
 
 // Launchers (defined in the .cu files); all enqueue on `stream`.
-cudaError_t launch_walk(SpecId id, bool static_f, const WalkParams& p, int blocks,
+// rearm: the variant that bounds each lane's next special node by R3's distance to F
+// (WalkParams::need3) instead of checking every step once armed.
+cudaError_t launch_walk(SpecId id, bool static_f, bool rearm, const WalkParams& p, int blocks,
                         cudaStream_t stream);
 int walk_blocks_per_sm(SpecId id, bool static_f);
 cudaError_t launch_init_stats(uint64_t* stats, uint64_t hist_lo, uint32_t hist_shift, uint32_t hist_bins,

@@ -364,8 +364,24 @@ __device__ __forceinline__ void park_lanes(const WalkParams& p, volatile WalkSha
   __syncwarp();
 }
 
+// Arm (check every step) once R3 is this close to F.  Whole-warp mode: lanes of a warp
+// walk in step and are checked together from the first armed one, so re-arming only pays
+// while it skips a long stretch (stride-1 walks: 2.8e6 checked steps per walk otherwise);
+// lane mode: lanes are independent, so a tight bound pays.
+constexpr uint64_t kArmSlackWarp = 1u << 16, kArmSlackLane = 1u << 10;
+constexpr uint64_t kArmBatch = 1u << 12;  // re-arm lanes due this soon in the same event
+
+// R3 of lane j (bits o3 .. o3 + l3 - 1 of its state).
+template <class S>
+__device__ __forceinline__ uint32_t lane_r3(const uint32_t (&s)[S::NB], int j) {
+  uint32_t r = 0;
+#pragma unroll
+  for (int i = 0; i < S::L3; ++i) r |= ((s[S::O3 + i] >> j) & 1u) << i;
+  return r;
+}
+
 // Events at the warp clock (rare): special nodes, arming, cap audits.
-template <class S, bool SF>
+template <class S, bool SF, bool RA>
 __device__ __forceinline__ void handle_events(const WalkParams& p, volatile WalkShared& sh,
                                               const uint32_t (&s)[S::NB]) {
   const uint32_t tid = tid_x(), w = tid >> 5;
@@ -409,10 +425,23 @@ __device__ __forceinline__ void handle_events(const WalkParams& p, volatile Walk
     }
   }
   if (next_arm <= t) {
+    // A lane due for arming first bounds its next possible special node: R3 reaches F
+    // only after need3[R3] more R3 clocks, at most one per step, so nothing can be
+    // reported before t + need3[R3].  Far-off lanes are re-armed there instead of being
+    // checked every step (the bound tightens ~4x per round, R3 clocking on ~3/4 of the
+    // steps); lanes due within kArmBatch are handled in the same event.
     next_arm = kInf;
+    const uint64_t slack = RA ? (sh.warp_mode ? kArmSlackWarp : kArmSlackLane) : 0u;
     for (uint32_t a = active & ~armed; a != 0u; a &= a - 1u) {
       const int j = __ffs(a) - 1;
-      const uint64_t at = meta[j].arm_at;
+      uint64_t at = meta[j].arm_at;
+      if (RA && at <= t + kArmBatch) {
+        const uint64_t need = p.need3 ? p.need3[lane_r3<S>(s, j)] : 0u;
+        if (need > slack && t + need > at) {
+          at = t + need;
+          meta[j].arm_at = at;
+        }
+      }
       if (at <= t) armed |= 1u << j;
       else next_arm = min(next_arm, at);
     }
@@ -439,8 +468,10 @@ __device__ __forceinline__ void handle_events(const WalkParams& p, volatile Walk
   sh.next_dead[tid] = next_dead;
 }
 
-template <class S, bool SF>
+template <class S, bool SF, bool RA>
 __global__ void __launch_bounds__(kWalkThreads, LC_WALK_MIN_BLOCKS) walk_kernel(const WalkParams p) {
+  // auto mode launches both variants; the one not meant for the probed mode exits
+  if (p.run_if_mode != ~0u && *p.mode_word != p.run_if_mode) return;
   __shared__ WalkShared sh_storage;
   volatile WalkShared& sh = sh_storage;
   {
@@ -518,7 +549,7 @@ __global__ void __launch_bounds__(kWalkThreads, LC_WALK_MIN_BLOCKS) walk_kernel(
       if (lane == 0) sh.t[w] = sh.t[w] + done;
       __syncwarp();
     }
-    handle_events<S, SF>(p, sh, s);
+    handle_events<S, SF, RA>(p, sh, s);
   }
 }
 
@@ -566,18 +597,21 @@ __global__ void mode_probe_kernel(const uint64_t* __restrict__ starts, uint64_t 
 }
 
 template <class S, bool SF>
-cudaError_t launch_t(const WalkParams& p, int blocks, cudaStream_t stream) {
-  walk_kernel<S, SF><<<blocks, kWalkThreads, 0, stream>>>(p);
+cudaError_t launch_t(const WalkParams& p, bool rearm, int blocks, cudaStream_t stream) {
+  if (rearm) walk_kernel<S, SF, true><<<blocks, kWalkThreads, 0, stream>>>(p);
+  else walk_kernel<S, SF, false><<<blocks, kWalkThreads, 0, stream>>>(p);
   return cudaGetLastError();
 }
 
 template <class S, bool SF>
 int occupancy_t() {
-  int b = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, walk_kernel<S, SF>, kWalkThreads, 0) !=
-      cudaSuccess)
+  int a = 0, b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, walk_kernel<S, SF, false>, kWalkThreads, 0) !=
+          cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, walk_kernel<S, SF, true>, kWalkThreads, 0) != cudaSuccess)
     return 1;
-  return b > 0 ? b : 1;
+  const int m = a < b ? a : b;
+  return m > 0 ? m : 1;
 }
 
 }  // namespace
@@ -613,17 +647,17 @@ cudaError_t launch_mode_probe(SpecId id, const uint64_t* starts, uint64_t n, uin
   return cudaGetLastError();
 }
 
-cudaError_t launch_walk(SpecId id, bool static_f, const WalkParams& p, int blocks,
+cudaError_t launch_walk(SpecId id, bool static_f, bool rearm, const WalkParams& p, int blocks,
                         cudaStream_t stream) {
   switch (id) {
     case SpecId::A51:
-      return static_f ? launch_t<A51, true>(p, blocks, stream) : launch_t<A51, false>(p, blocks, stream);
+      return static_f ? launch_t<A51, true>(p, rearm, blocks, stream) : launch_t<A51, false>(p, rearm, blocks, stream);
     case SpecId::MINI567:
-      return static_f ? launch_t<MINI567, true>(p, blocks, stream)
-                      : launch_t<MINI567, false>(p, blocks, stream);
+      return static_f ? launch_t<MINI567, true>(p, rearm, blocks, stream)
+                      : launch_t<MINI567, false>(p, rearm, blocks, stream);
     case SpecId::MINI789:
-      return static_f ? launch_t<MINI789, true>(p, blocks, stream)
-                      : launch_t<MINI789, false>(p, blocks, stream);
+      return static_f ? launch_t<MINI789, true>(p, rearm, blocks, stream)
+                      : launch_t<MINI789, false>(p, rearm, blocks, stream);
     default:
       return cudaErrorInvalidValue;
   }
