@@ -323,7 +323,9 @@ def main() -> None:
             "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": value / PAPER_GTX580,
             "vs_baseline_ref": "paper GTX 580 bitsliced walk, 9,800 nodes/s x 11.17e6 clocks (PAPER.md:478-479)",
-            "dtype": "u32 (bitsliced words, 32 lanes)", "data": "synthetic (K0 seeded special A5/1 nodes)",
+            "dtype": "u32 (bitsliced words, 32 lanes)",
+            "data": "synthetic (" + ("K0 seeded special A5/1 nodes" if args.starts == "k0"
+                                     else "seeded uniform random valid A5/1 states") + ")",
             "config": {"workload": f"configs[1]: 2^{args.workload_log2} "
                                    f"{'special A5/1 start nodes' if args.starts == 'k0' else 'uniform random A5/1 states'}"
                                    f" per GPU, walked {LEGS} hop(s) to the next special node, stride {STRIDE_}; "
