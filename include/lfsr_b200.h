@@ -215,6 +215,33 @@ int lc_count_cycles(lc_ctx *ctx, uint64_t n, const uint64_t *src, const uint64_t
                     uint64_t *hop_count, uint64_t *clock_length, uint64_t *tree_size,
                     uint64_t *n_cycles);
 
+/* ------------------------- exhaustive mini-cipher analysis (oracle.py:141-283) */
+
+/* The building blocks of the reference's ground-truth oracle brute_force_analysis, on
+ * the GPU (device buffers, rank-encoded states as oracle.py:55-63).  n must be the spec's
+ * valid state count (< 2^31).  build: successor ranks (majority rule, or every register
+ * clocked when clock_all), in-degrees, candidate flags (R3 == F, successor's R3 != F,
+ * in-degree > 0) and cycle_of[i] = f^(2^k)(i), an on-cycle state of i's component. */
+int lc_bf_build_device(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3, int clock_all, uint64_t n,
+                       int64_t *d_succ, int32_t *d_indeg, uint8_t *d_is_cand, int64_t *d_cycle_of,
+                       void *stream);
+/* Candidate-graph edges: each of the m candidate ranks walked through the successor map
+ * to the first candidate (dst rank, distance). */
+int lc_bf_edges_device(lc_ctx *ctx, uint64_t n, const int64_t *d_succ, const uint8_t *d_is_cand,
+                       const int64_t *d_cand, uint64_t m, int64_t *d_dst, int64_t *d_dist, void *stream);
+/* Segment sweep from the ascending candidate ranks: root[i] = index of i's candidate
+ * (or -1), depth[i]; level_counts[l] = states at depth l (host array, level_cap entries;
+ * *n_levels = levels found).  Synchronous. */
+int lc_bf_segments_device(lc_ctx *ctx, uint64_t n, const int64_t *d_succ, const int32_t *d_indeg,
+                          const uint8_t *d_is_cand, const int64_t *d_cand, uint64_t ncand, int64_t *d_root,
+                          int32_t *d_depth, uint64_t *level_counts, uint32_t level_cap, uint32_t *n_levels,
+                          void *stream);
+/* Cycles of a permutation of m compact indices (cs[i] = successor's index; indices in
+ * ascending state order): start[i] = smallest index on i's cycle, steps[i] = steps from
+ * i forward to it. */
+int lc_bf_cycle_order_device(lc_ctx *ctx, uint64_t m, const int64_t *d_cs, int64_t *d_start,
+                             int64_t *d_steps, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

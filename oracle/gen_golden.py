@@ -12,6 +12,7 @@ Usage (from the repo root, in the build container):
     python oracle/gen_golden.py enumerate  # ~30 s: A5/1 step-1 sub-slice digest
     python oracle/gen_golden.py kat        # ~2 min: A5/1 seed-0 256-walk known answer
     python oracle/gen_golden.py reduce     # ~1 min: steps 4-5 (leaf cutting, cycles) on minis
+    python oracle/gen_golden.py bruteforce # ~2 min: the reference's exhaustive mini analysis
     python oracle/gen_golden.py c1 [W]     # ~1 h on 8 cores: the full 2^16 config-1 set
 
 Digest format: sha256 over lines
@@ -450,6 +451,34 @@ def gen_c1(ref, workers):
          dst=dst[::256], dist=dist[::256])
 
 
+def gen_bruteforce(ref):
+    """oracle.brute_force_analysis (oracle.py:141-283) on the minis, majority and
+    clock-all dynamics: summaries, cycles, histograms and digests of every array."""
+    out = {}
+    for name in ("MINI567", "MINI789"):
+        spec = getattr(ref.cipher, name)
+        params = ref.cipher.CandidateParams.from_spec(spec, ref.cipher.default_fixed_r3(spec))
+        for clock_all in (False, True):
+            t0 = time.perf_counter()
+            gt = ref.oracle.brute_force_analysis(spec, params, clock_all=clock_all)
+            el = time.perf_counter() - t0
+            cycles = sorted((c.leader, c.clock_length, c.candidate_count, c.component_size) for c in gt.cycles)
+            members = np.concatenate([c.ranks for c in sorted(gt.cycles, key=lambda c: int(c.ranks[0]))]) \
+                if gt.cycles else np.zeros(0, dtype=np.int64)
+            out[f"{name.lower()}_{'clockall' if clock_all else 'majority'}"] = {
+                "summary": gt.summary(), "pred_count_hist": gt.pred_count_hist.tolist(),
+                "cycles": [list(map(int, c)) for c in cycles],
+                "cycle_members_digest": u64_digest(members),
+                "level_counts": gt.level_counts.tolist(),
+                "succ_digest": u64_digest(gt.succ), "cand_ranks_digest": u64_digest(gt.cand_ranks),
+                "edge_dst_digest": u64_digest(gt.edge_dst), "edge_dist_digest": u64_digest(gt.edge_dist),
+                "seg_depth_digest": u64_digest(gt.seg_depth), "seg_size_digest": u64_digest(gt.seg_size),
+                "seconds": el,
+            }
+            print(name, clock_all, gt.summary(), f"{el:.1f}s", flush=True)
+    save_json("bruteforce.json", out)
+
+
 def main():
     ref = ref_shim.load()
     what = sys.argv[1] if len(sys.argv) > 1 else "basic"
@@ -466,6 +495,8 @@ def main():
         gen_reduce(ref)
     elif what == "tuning":
         gen_tuning(ref)
+    elif what == "bruteforce":
+        gen_bruteforce(ref)
     elif what == "c1":
         gen_c1(ref, int(sys.argv[2]) if len(sys.argv) > 2 else os.cpu_count())
     else:

@@ -91,6 +91,12 @@ _SIGNATURES = {
     "lc_cut_shard_apply": ([_vp, C.c_int, _vp, C.c_uint64], C.c_int),
     "lc_cut_shard_finish": ([_vp, _u64p], C.c_int),
     "lc_cut_shard_destroy": ([_vp], C.c_int),
+    "lc_bf_build_device": ([_vp, C.POINTER(lc_spec), C.c_uint64, C.c_int, C.c_uint64, _vp, _vp, _vp, _vp, _vp],
+                           C.c_int),
+    "lc_bf_edges_device": ([_vp, C.c_uint64, _vp, _vp, _vp, C.c_uint64, _vp, _vp, _vp], C.c_int),
+    "lc_bf_segments_device": ([_vp, C.c_uint64, _vp, _vp, _vp, _vp, C.c_uint64, _vp, _vp, _u64p, C.c_uint32,
+                               C.POINTER(C.c_uint32), _vp], C.c_int),
+    "lc_bf_cycle_order_device": ([_vp, C.c_uint64, _vp, _vp, _vp, _vp], C.c_int),
     "lc_count_cycles": ([_vp, C.c_uint64, _u64p, _u64p, _u64p, _u64p, _u64p, _u64p, _u64p, _u64p, _u64p],
                         C.c_int),
 }

@@ -862,6 +862,81 @@ int lc_cut_shard_destroy(lc_cut_shard* h) {
   return LC_OK;
 }
 
+// ------------------------------------------------ exhaustive mini-cipher analysis
+
+static uint64_t valid_states(lc::SpecId id) {
+  switch (id) {
+    case lc::SpecId::A51: return ((1ull << 19) - 1) * ((1ull << 22) - 1) * ((1ull << 23) - 1);
+    case lc::SpecId::MINI567: return 31ull * 63ull * 127ull;
+    case lc::SpecId::MINI789: return 127ull * 255ull * 511ull;
+    default: return 0;
+  }
+}
+
+int lc_bf_build_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int clock_all, uint64_t n,
+                       int64_t* d_succ, int32_t* d_indeg, uint8_t* d_is_cand, int64_t* d_cycle_of, void* stream) {
+  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  lc::SpecId id;
+  int rc = check_spec(spec, &id);
+  if (rc) return rc;
+  if ((rc = check_fixed(id, fixed_r3))) return rc;
+  if (n != valid_states(id)) return fail(LC_ERR_ARG, "n must be the spec's valid state count");
+  if (n > (1ull << 31)) return fail(LC_ERR_ARG, "instance too large for exhaustive analysis");
+  if (!d_succ || !d_indeg || !d_is_cand || !d_cycle_of) return fail(LC_ERR_ARG, "null buffer");
+  LC_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  LC_CUDA(ctx->scratch.ensure(n * 8));
+  int launches = 0;
+  LC_CUDA(lc::bf_build(id, n, clock_all, static_cast<uint32_t>(fixed_r3), d_succ, d_indeg, d_is_cand, d_cycle_of,
+                       ctx->scratch.as<int64_t>(), st, &launches));
+  g_launches += launches;
+  return LC_OK;
+}
+
+int lc_bf_edges_device(lc_ctx* ctx, uint64_t n, const int64_t* d_succ, const uint8_t* d_is_cand,
+                       const int64_t* d_cand, uint64_t m, int64_t* d_dst, int64_t* d_dist, void* stream) {
+  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  if (m && (!d_succ || !d_is_cand || !d_cand || !d_dst || !d_dist)) return fail(LC_ERR_ARG, "null buffer");
+  LC_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  int launches = 0;
+  LC_CUDA(lc::bf_edges(n, d_succ, d_is_cand, d_cand, m, d_dst, d_dist, st, &launches));
+  g_launches += launches;
+  return LC_OK;
+}
+
+int lc_bf_segments_device(lc_ctx* ctx, uint64_t n, const int64_t* d_succ, const int32_t* d_indeg,
+                          const uint8_t* d_is_cand, const int64_t* d_cand, uint64_t ncand, int64_t* d_root,
+                          int32_t* d_depth, uint64_t* level_counts, uint32_t level_cap, uint32_t* n_levels,
+                          void* stream) {
+  if (!ctx || !n_levels || (level_cap && !level_counts)) return fail(LC_ERR_ARG, "null argument");
+  if (!d_succ || !d_indeg || !d_is_cand || !d_root || !d_depth || (ncand && !d_cand))
+    return fail(LC_ERR_ARG, "null buffer");
+  LC_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  const size_t bytes = lc::bf_segments_scratch(n);
+  LC_CUDA(ctx->scratch.ensure(bytes));
+  int launches = 0;
+  LC_CUDA(lc::bf_segments(n, d_succ, d_indeg, d_is_cand, d_cand, ncand, d_root, d_depth, level_counts, level_cap,
+                          n_levels, ctx->scratch.p, ctx->scratch.bytes, st, &launches));
+  g_launches += launches;
+  return LC_OK;
+}
+
+int lc_bf_cycle_order_device(lc_ctx* ctx, uint64_t m, const int64_t* d_cs, int64_t* d_start, int64_t* d_steps,
+                             void* stream) {
+  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  if (m && (!d_cs || !d_start || !d_steps)) return fail(LC_ERR_ARG, "null buffer");
+  LC_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  LC_CUDA(ctx->scratch.ensure(std::max<uint64_t>(m, 1) * 8 * 3));
+  int64_t* t = ctx->scratch.as<int64_t>();
+  int launches = 0;
+  LC_CUDA(lc::bf_cycle_order(m, d_cs, d_start, d_steps, t, t + m, t + 2 * m, st, &launches));
+  g_launches += launches;
+  return LC_OK;
+}
+
 int lc_count_cycles(lc_ctx* ctx, uint64_t n, const uint64_t* src, const uint64_t* dst, const uint64_t* dist,
                     const uint64_t* subtree_size, uint64_t* leader, uint64_t* hop_count, uint64_t* clock_length,
                     uint64_t* tree_size, uint64_t* n_cycles) {

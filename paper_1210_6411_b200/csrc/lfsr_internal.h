@@ -154,6 +154,19 @@ cudaError_t shard_apply(ShardState* sh, int phase, const uint64_t* msgs, uint64_
 cudaError_t shard_finish(ShardState* sh, uint64_t* n_out, unsigned int* err_out, cudaStream_t st, int* launches);
 constexpr uint32_t kMaxShardRanks = 1024;
 
+// Exhaustive mini-cipher analysis (bruteforce.cu; oracle.brute_force_analysis).
+cudaError_t bf_build(SpecId id, uint64_t n, int clock_all, uint32_t F, int64_t* succ, int32_t* indeg,
+                     uint8_t* is_cand, int64_t* g, int64_t* tmp, cudaStream_t st, int* launches);
+cudaError_t bf_edges(uint64_t n, const int64_t* succ, const uint8_t* is_cand, const int64_t* cand, uint64_t m,
+                     int64_t* dst, int64_t* dist, cudaStream_t st, int* launches);
+size_t bf_segments_scratch(uint64_t n);
+cudaError_t bf_segments(uint64_t n, const int64_t* succ, const int32_t* indeg, const uint8_t* is_cand,
+                        const int64_t* cand, uint64_t ncand, int64_t* root, int32_t* depth, uint64_t* level_counts,
+                        uint32_t level_cap, uint32_t* n_levels, void* scratch, size_t scratch_bytes, cudaStream_t st,
+                        int* launches);
+cudaError_t bf_cycle_order(uint64_t m, const int64_t* cs, int64_t* lab, int64_t* steps, int64_t* t0, int64_t* t1,
+                           int64_t* t2, cudaStream_t st, int* launches);
+
 size_t cycles_scratch_bytes(uint64_t n);
 cudaError_t count_cycles_device(uint64_t n, const uint64_t* src, const uint64_t* dst, const uint64_t* dist,
                                 const uint64_t* size, uint64_t* leader, uint64_t* hops_out, uint64_t* clocks_out,
