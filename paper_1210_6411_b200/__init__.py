@@ -25,5 +25,8 @@ from .records import (EDGE_SIZE, ByteCounter, EdgeRecord, read_edge_arrays, read
 from .reduce import (CycleRecord, IterationLog, NotAPermutationError, PassStats,  # noqa: F401
                      ReduceConfig, count_cycles, count_cycles_arrays, cut_leaves_arrays,
                      cut_leaves_pass, cut_leaves_to_fixpoint, sort_edge_arrays)
+from .ground_truth import CycleInfo, GroundTruth, brute_force_analysis  # noqa: F401
+from .stats import (AnalysisReport, ExpectationTable, SampleStats, deviation_report,  # noqa: F401
+                    random_mapping_expectations, sample_segment_distances, sample_segment_shapes)
 
 __version__ = "0.1.0"

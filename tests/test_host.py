@@ -235,3 +235,18 @@ def test_prune_config_validation_matches_reference(lc):
         except ValueError:
             got = "ValueError"
         assert got == want, key
+
+
+def test_package_exports_reference_namespace():
+    """Every name the reference package exports (pkg/src/lfsrcycles/__init__.py:3-32)."""
+    import paper_1210_6411_b200 as pkg
+
+    names = ("A51 MINI567 MINI789 CandidateParams CipherSpec PredecessorTable build_predecessor_table "
+             "builtin_spec clock_forward default_fixed_r3 expected_chain_count expected_chain_length "
+             "is_candidate majority_clock_mask minimum_cycle_length predecessors SlicedBatch calibrate_stride "
+             "clock_sliced forward_to_candidate transpose untranspose PruneConfig build_skeleton_edges "
+             "enumerate_candidates prune_shallow_segments EdgeRecord CycleRecord ReduceConfig count_cycles "
+             "cut_leaves_pass cut_leaves_to_fixpoint GroundTruth brute_force_analysis AnalysisReport "
+             "ExpectationTable SampleStats deviation_report random_mapping_expectations "
+             "sample_segment_distances sample_segment_shapes").split()
+    assert [n for n in names if not hasattr(pkg, n)] == []
