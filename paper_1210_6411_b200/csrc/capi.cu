@@ -691,6 +691,14 @@ static int reduce_error(unsigned int err) {
   }
 }
 
+// An empty edge list: one pass that removes nothing, as the reference logs it
+// (reduce.py:189-223 runs cut_leaves_pass once before testing for the fixpoint).
+static int empty_cut(uint64_t* pass_stats, uint32_t max_stats, uint32_t* n_passes) {
+  *n_passes = 1;
+  if (max_stats && pass_stats) pass_stats[0] = pass_stats[1] = pass_stats[2] = 0;
+  return LC_OK;
+}
+
 int lc_sort_edges(lc_ctx* ctx, uint64_t n, uint64_t* src, uint64_t* dst, uint64_t* dist, uint64_t* subtree_size,
                   uint64_t* subtree_depth) {
   if (!ctx) return fail(LC_ERR_ARG, "null context");
@@ -723,7 +731,7 @@ int lc_cut_leaves(lc_ctx* ctx, uint64_t n, uint64_t* src, uint64_t* dst, uint64_
   if (!ctx || !n_passes || !n_out) return fail(LC_ERR_ARG, "null argument");
   *n_passes = 0;
   *n_out = n;
-  if (n == 0) return LC_OK;
+  if (n == 0) return empty_cut(pass_stats, max_stats, n_passes);
   if (!src || !dst || !dist || !subtree_size || !subtree_depth) return fail(LC_ERR_ARG, "null buffer");
   LC_CUDA(cudaSetDevice(ctx->device));
   const size_t nb = n * 8;
@@ -753,9 +761,9 @@ int lc_cut_leaves_device(lc_ctx* ctx, uint64_t n, uint64_t* src, uint64_t* dst, 
   if (!ctx || !n_passes || !n_out) return fail(LC_ERR_ARG, "null argument");
   *n_passes = 0;
   *n_out = n;
-  if (n == 0) return LC_OK;
-  if (!src || !dst || !dist || !subtree_size || !subtree_depth) return fail(LC_ERR_ARG, "null buffer");
   if (max_stats && !pass_stats) return fail(LC_ERR_ARG, "null pass_stats");
+  if (n == 0) return empty_cut(pass_stats, max_stats, n_passes);
+  if (!src || !dst || !dist || !subtree_size || !subtree_depth) return fail(LC_ERR_ARG, "null buffer");
   LC_CUDA(cudaSetDevice(ctx->device));
   // The passes are replayed from a CUDA graph, which cannot be captured on the legacy
   // default stream: wait for the caller's stream, then run on the context's own stream

@@ -1,0 +1,56 @@
+"""Empty and minimal inputs through the public API, against the reference's behaviour on
+the same inputs (recorded here from runs of the reference in the build container):
+empty edge files (one pass that removes nothing), a single self-loop record, empty
+candidate lists, empty walks and empty sliced batches."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_empty_and_self_loop_reduce(gpu, lc, tmp_path):
+    from paper_1210_6411_b200 import reduce as R
+    from paper_1210_6411_b200.records import EdgeRecord, read_edges, write_edges
+
+    cfg = R.ReduceConfig()
+    p, q = tmp_path / "e.bin", tmp_path / "o.bin"
+    write_edges(p, [])
+    st = R.cut_leaves_pass(p, q, cfg)
+    assert (st.leaves_removed, st.inner_nodes, st.out_size_sum) == (0, 0, 0)
+    log = R.cut_leaves_to_fixpoint(p, q, cfg)
+    assert [(s.leaves_removed, s.inner_nodes, s.out_size_sum) for s in log.passes] == [(0, 0, 0)]
+    assert log.iterations == 0 and list(read_edges(q)) == []
+    assert R.count_cycles([]) == [] and R.count_cycles(str(q)) == []
+    write_edges(p, [EdgeRecord(5, 5, 7, 0, 0)])
+    log = R.cut_leaves_to_fixpoint(p, q, cfg)
+    assert [(s.leaves_removed, s.inner_nodes, s.out_size_sum) for s in log.passes] == [(0, 1, 0)]
+    assert list(read_edges(q)) == [EdgeRecord(5, 5, 7, 0, 0)]
+    assert R.count_cycles(list(read_edges(q))) == [R.CycleRecord(5, 1, 7, 0)]
+
+
+def test_empty_candidate_lists(gpu, lc, specs, params):
+    spec, prm = specs["mini567"], params["mini567"]
+    surv, st = lc.prune_shallow_segments([], lc.PruneConfig(depth_limit=10), spec, prm)
+    assert surv == [] and (st.mode, st.limit, st.total, st.removed, st.expanded) == ("dfs", 10, 0, 0, 0)
+    assert lc.forward_to_candidate([], prm, spec) == []
+    from paper_1210_6411_b200.bitslice import candidate_hops
+
+    assert candidate_hops([], prm, spec) == []
+    sb = lc.transpose([], spec, 64)
+    filler = spec.pack(1, 1, 1)  # every lane of an empty batch is a filler (bitslice.py:46, :71-77)
+    assert sb.words == [(1 << 64) - 1 if (filler >> i) & 1 else 0 for i in range(spec.total_bits)]
+    assert sb.lane_count == 0 and lc.untranspose(lc.clock_sliced(sb, spec, 5)) == []
+    empty = np.zeros(0, dtype=np.uint64)
+    assert lc.is_candidate(empty, prm, spec).size == 0
+    assert lc.enumerate_candidates_array(spec, prm, 5, 5).size == 0
+
+
+def test_cut_leaves_arrays_empty(gpu, lc):
+    z = np.zeros(0, dtype=np.uint64)
+    out = lc.cut_leaves_arrays(z, z, z, z, z)
+    assert out[5] == [(0, 0, 0)] and all(c.size == 0 for c in out[:5])
+    out = lc.cut_leaves_arrays(z, z, z, z, z, max_passes=1)
+    assert out[5] == [(0, 0, 0)]
