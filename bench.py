@@ -40,7 +40,7 @@ CAP = 178_957_008  # the reference's default walk cap for A5/1 (bitslice.py:273-
 PAPER_SCALE_TRANSITIONS = int(2 ** 33.6 * 11_184_857)  # ~1.46e17
 # DRAM bytes per walk of the walk kernel: dram__bytes_read.sum + dram__bytes_write.sum of
 # one ncu capture (profiles/r01_walk_a51_metrics.json, a 2^20-walk launch) / walks
-TRAFFIC_BYTES_PER_WALK = (9.219072e6 + 21.899008e6) / (1 << 20)
+TRAFFIC_BYTES_PER_WALK = (9.564160e6 + 47.801344e6) / (1 << 20)
 
 
 def host_cores() -> int:
