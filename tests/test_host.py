@@ -250,3 +250,16 @@ def test_package_exports_reference_namespace():
              "ExpectationTable SampleStats deviation_report random_mapping_expectations "
              "sample_segment_distances sample_segment_shapes").split()
     assert [n for n in names if not hasattr(pkg, n)] == []
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: without the CUDA library the package import raises ImportError."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, LFSR_LIB=str(tmp_path / "missing.so"))
+    code = "import paper_1210_6411_b200"
+    r = subprocess.run([sys.executable, "-c", code], cwd=os.path.dirname(os.path.dirname(__file__)), env=env,
+                       capture_output=True, text=True)
+    assert r.returncode != 0 and "ImportError" in r.stderr and "no CPU fallback" in r.stderr.replace("There is no", "no")
