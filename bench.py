@@ -166,9 +166,18 @@ def main() -> None:
     import torch
     import torch.distributed as dist
 
+    # LFSR_BENCH_SHARE_GPU=1 (testing only): every rank on cuda:0 with gloo, to exercise the
+    # multi-rank path on a one-GPU box (the walks are independent; the only collectives
+    # are the barriers and the statistics all-reduce outside the timed region)
+    share = os.environ.get("LFSR_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_1210_6411_b200 as lc
     from paper_1210_6411_b200 import _native as N
