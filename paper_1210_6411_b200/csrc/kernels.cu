@@ -435,6 +435,7 @@ __device__ __forceinline__ uint64_t child_of(uint64_t y, int q) {
 // the stackless climb, which rediscovers them (and an empty ring without overflow means
 // the traversal is complete -- no climb back to the root).
 constexpr int kRing = 8;
+constexpr int kTailBurst = 32;  // steps per warp vote once no candidate is left to take
 
 struct Ring {
   uint32_t* lo;  // [kRing][kThreads]: node low word
@@ -575,7 +576,13 @@ __global__ void __launch_bounds__(kThreads) prune_kernel(const uint64_t* __restr
     }
     if (!__any_sync(kFull, have)) break;
     if (have) {
-      const int r = prune_step<S>(x, d, acc, climb, ring, F, mode, limit);
+      // once the candidates are drained nothing can be refilled: run bursts of steps
+      // between warp votes (the tail is latency-bound on the longest traversals)
+      int r = prune_step<S>(x, d, acc, climb, ring, F, mode, limit);
+      if (drained) {
+#pragma unroll 1
+        for (int k = 1; k < kTailBurst && r == 0; ++k) r = prune_step<S>(x, d, acc, climb, ring, F, mode, limit);
+      }
       if (r != 0) {
         removed[i] = r == 1 ? 1 : 0;
         work[i] = acc;
