@@ -458,82 +458,101 @@ struct Ring {
   }
 };
 
+// The child mask of x alone (expand_node without building the children): the table
+// entry, minus the rare special-node children (only when unstep(R3(x)) == F).
+template <class S>
+__device__ __forceinline__ uint32_t child_mask(uint64_t x, uint32_t F) {
+  uint32_t m = pattern_set(table_index<S>(x));
+  const uint32_t r3 = static_cast<uint32_t>((x >> S::O3) & S::M3);
+  if (unstep<S::L3, S::T3>(r3) == F) {
+#pragma unroll
+    for (int q = 1; q < 4; ++q)
+      if (((m >> q) & 1u) && ((kNonEmpty >> table_index<S>(child_of<S>(x, q))) & 1ull)) m &= ~(1u << q);
+  }
+  return m;
+}
+
 // One traversal step of a candidate's segment: exactly one node expansion per step for
-// every lane (uniform across the warp).  State: x (the node to expand next), d (its
-// depth), acc (expanded for dfs / node count for bfs), climb (x's subtree is finished and
-// the ring lost entries: this step expands x's parent to find x's next-lower sibling).
+// every lane.  State: x (the node to expand next), d (its depth), acc (expanded for dfs /
+// node count for bfs), climb (x's subtree is finished and the ring lost entries: this
+// step expands x's parent to find x's next-lower sibling -- rare).  The two common cases
+// (descend into x's highest child; or, at a leaf, resume the deepest pending branch
+// point) only pick the source node and child index, then share one child computation,
+// so a warp's lanes diverge only over a few selects and the ring access.
 // Returns 0 while running, 1 = finished shallow, 2 = finished deep (not shallow).
 template <class S>
 __device__ __forceinline__ int prune_step(uint64_t& x, uint64_t& d, uint64_t& acc, bool& climb, Ring& ring,
                                           uint32_t F, int mode, uint64_t limit) {
-  uint64_t y = x;
-  if (climb) y = clock_scalar<S>(x);  // x's parent
-  const Node<S> nd = expand_node<S>(y, F);
-  bool leaf;
+  uint64_t src = x;
+  uint32_t q = 0;
+  bool finished;  // x's subtree is done: continue from the ring (or climb)
   if (!climb) {
-    leaf = nd.mask == 0u;
-    if (!leaf) {
+    const uint32_t m = child_mask<S>(x, F);
+    finished = m == 0u;
+    if (!finished) {
       if (mode == 0) {
         if (d >= limit) {  // a child would sit below the depth limit
           acc += 1;
           return 2;
         }
-        acc += __popc(nd.mask);
+        acc += __popc(m);
       } else {
-        acc += __popc(nd.mask);
+        acc += __popc(m);
         if (acc > limit) {
           acc = limit + 1;
           return 2;
         }
       }
-      const int q = 31 - __clz(nd.mask);  // the reference pops the last child first
-      const uint32_t rest = nd.mask & ~(1u << q);
+      q = 31 - __clz(m);  // the reference pops the last child first
+      const uint32_t rest = m & ~(1u << q);
       if (rest) ring.push(x, d, rest);
-      x = nd.child(q);
       ++d;
-      return 0;
     }
   } else {
-    // continue with x's next-lower sibling, else keep climbing
-    uint32_t q = 0;
+    // x's parent y: continue with x's next-lower sibling, else y's subtree is done too
+    const uint64_t y = clock_scalar<S>(x);
+    const Node<S> nd = expand_node<S>(y, F);
+    uint32_t k = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (((nd.mask >> k) & 1u) && nd.child(k) == x) q = k;
-    const uint32_t lower = nd.mask & ((1u << q) - 1u);
-    if (lower != 0u) {
-      const int c = 31 - __clz(lower);
-      const uint32_t rest = lower & ~(1u << c);
+    for (int c = 0; c < 4; ++c)
+      if (((nd.mask >> c) & 1u) && nd.child(c) == x) k = c;
+    const uint32_t lower = nd.mask & ((1u << k) - 1u);
+    finished = lower == 0u;
+    if (finished) {
+      x = y;
+      --d;
+    } else {
+      q = 31 - __clz(lower);
+      const uint32_t rest = lower & ~(1u << q);
       if (rest) ring.push(y, d - 1, rest);
-      x = nd.child(c);
+      src = y;
       climb = false;
+    }
+  }
+  if (finished) {
+    if (ring.cnt) {  // resume the deepest pending branch point
+      const uint32_t slot = ring.at(ring.top);
+      src = static_cast<uint64_t>(ring.lo[slot]) | (static_cast<uint64_t>(ring.hi[slot]) << 32);
+      const uint32_t dm = ring.dm[slot];
+      const uint32_t mask = dm & 15u;
+      q = 31 - __clz(mask);
+      const uint32_t rest = mask & ~(1u << q);
+      if (rest) {
+        ring.dm[slot] = (dm & ~15u) | rest;
+      } else {
+        ring.top = (ring.top - 1) & (kRing - 1);
+        --ring.cnt;
+      }
+      d = (dm >> 4) + 1;
+      climb = false;
+    } else if (!ring.lost || d == 0) {
+      return 1;  // nothing pending: traversal complete
+    } else {
+      climb = true;
       return 0;
     }
-    x = y;
-    --d;
-    leaf = true;  // y's subtree is finished too
   }
-  // x's subtree is finished: resume the deepest pending branch point
-  if (ring.cnt) {
-    const uint32_t slot = ring.at(ring.top);
-    const uint64_t p = static_cast<uint64_t>(ring.lo[slot]) | (static_cast<uint64_t>(ring.hi[slot]) << 32);
-    const uint32_t dm = ring.dm[slot];
-    const uint32_t mask = dm & 15u;
-    const int q = 31 - __clz(mask);
-    const uint32_t rest = mask & ~(1u << q);
-    if (rest) {
-      ring.dm[slot] = (dm & ~15u) | rest;
-    } else {
-      ring.top = (ring.top - 1) & (kRing - 1);
-      --ring.cnt;
-    }
-    x = child_of<S>(p, q);
-    d = (dm >> 4) + 1;
-    climb = false;
-    return 0;
-  }
-  if (!ring.lost || d == 0) return 1;  // nothing pending: traversal complete
-  climb = true;
-  (void)leaf;
+  x = child_of<S>(src, q);  // one child computation shared by descend / sibling / resume
   return 0;
 }
 
