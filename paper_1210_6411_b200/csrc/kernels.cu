@@ -434,16 +434,23 @@ __device__ __forceinline__ uint64_t child_of(uint64_t y, int q) {
 // overflowed, the oldest entries are gone; once it runs empty the traversal falls back to
 // the stackless climb, which rediscovers them (and an empty ring without overflow means
 // the traversal is complete -- no climb back to the root).
-constexpr int kRing = 8;
+#ifndef LC_PRUNE_RING
+#define LC_PRUNE_RING 32
+#endif
+#ifndef LC_PRUNE_THREADS
+#define LC_PRUNE_THREADS 128
+#endif
+constexpr int kRing = LC_PRUNE_RING;
+constexpr int kPruneThreads = LC_PRUNE_THREADS;  // the ring takes kRing * 12 B per thread of shared memory
 constexpr int kTailBurst = 32;  // steps per warp vote once no candidate is left to take
 
 struct Ring {
-  uint32_t* lo;  // [kRing][kThreads]: node low word
+  uint32_t* lo;  // [kRing][kPruneThreads]: node low word
   uint32_t* hi;  //                   node high word
   uint32_t* dm;  //                   depth << 4 | remaining child mask
   uint32_t top, cnt;
   bool lost;
-  __device__ __forceinline__ uint32_t at(uint32_t slot) const { return slot * kThreads + threadIdx.x; }
+  __device__ __forceinline__ uint32_t at(uint32_t slot) const { return slot * kPruneThreads + threadIdx.x; }
   __device__ __forceinline__ void push(uint64_t y, uint64_t d, uint32_t mask) {
     if (d >= (1ull << 27)) {  // depth does not fit the slot: leave it to the stackless climb
       lost = true;
@@ -509,14 +516,16 @@ __device__ __forceinline__ int prune_step(uint64_t& x, uint64_t& d, uint64_t& ac
       ++d;
     }
   } else {
-    // x's parent y: continue with x's next-lower sibling, else y's subtree is done too
+    // x's parent y: continue with x's next-lower sibling, else y's subtree is done too.
+    // x's child index follows from which registers differ between x and y (the clocked
+    // ones: a maximal-period register step has no nonzero fixed point), so no child of y
+    // has to be built to find it.
     const uint64_t y = clock_scalar<S>(x);
-    const Node<S> nd = expand_node<S>(y, F);
-    uint32_t k = 0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-      if (((nd.mask >> c) & 1u) && nd.child(c) == x) k = c;
-    const uint32_t lower = nd.mask & ((1u << k) - 1u);
+    const uint64_t diff = x ^ y;
+    const uint32_t pat = ((diff & S::M1) ? 1u : 0u) | (((diff >> S::O2) & S::M2) ? 2u : 0u) |
+                         (((diff >> S::O3) & S::M3) ? 4u : 0u);
+    const uint32_t k = pat == 3u ? 0u : pat == 5u ? 1u : pat == 6u ? 2u : 3u;  // clock_pattern^-1
+    const uint32_t lower = child_mask<S>(y, F) & ((1u << k) - 1u);
     finished = lower == 0u;
     if (finished) {
       x = y;
@@ -560,12 +569,12 @@ __device__ __forceinline__ int prune_step(uint64_t& x, uint64_t& d, uint64_t& ac
 // it finishes (tickets aggregated over the lanes that need one), so a warp is never held
 // up by its deepest segment.
 template <class S>
-__global__ void __launch_bounds__(kThreads) prune_kernel(const uint64_t* __restrict__ cands, uint64_t n,
+__global__ void __launch_bounds__(kPruneThreads) prune_kernel(const uint64_t* __restrict__ cands, uint64_t n,
                                                          uint32_t F, int mode, uint64_t limit,
                                                          uint8_t* __restrict__ removed,
                                                          uint64_t* __restrict__ work,
                                                          unsigned long long* queue) {
-  __shared__ uint32_t ring_lo[kRing * kThreads], ring_hi[kRing * kThreads], ring_dm[kRing * kThreads];
+  __shared__ uint32_t ring_lo[kRing * kPruneThreads], ring_hi[kRing * kPruneThreads], ring_dm[kRing * kPruneThreads];
   const uint32_t lane = threadIdx.x & 31u;
   uint64_t i = 0, x = 0, d = 0, acc = 0;
   bool have = false, climb = false, drained = false;
@@ -686,7 +695,7 @@ cudaError_t launch_random_candidates(SpecId id, uint32_t F, uint64_t seed, uint6
 cudaError_t launch_prune(SpecId id, uint32_t F, int mode, uint64_t limit, const uint64_t* cands,
                          uint64_t n, uint8_t* removed, uint64_t* work, unsigned long long* queue,
                          int blocks, cudaStream_t stream) {
-  LC_DISPATCH(id, prune_kernel<S><<<blocks, kThreads, 0, stream>>>(cands, n, F, mode, limit, removed, work,
+  LC_DISPATCH(id, prune_kernel<S><<<blocks, kPruneThreads, 0, stream>>>(cands, n, F, mode, limit, removed, work,
                                                                    queue);
               return cudaGetLastError());
 }
@@ -694,9 +703,9 @@ cudaError_t launch_prune(SpecId id, uint32_t F, int mode, uint64_t limit, const 
 int prune_blocks_per_sm(SpecId id) {
   int b = 1;
   switch (id) {
-    case SpecId::A51: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, prune_kernel<A51>, kThreads, 0); break;
-    case SpecId::MINI567: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, prune_kernel<MINI567>, kThreads, 0); break;
-    case SpecId::MINI789: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, prune_kernel<MINI789>, kThreads, 0); break;
+    case SpecId::A51: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, prune_kernel<A51>, kPruneThreads, 0); break;
+    case SpecId::MINI567: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, prune_kernel<MINI567>, kPruneThreads, 0); break;
+    case SpecId::MINI789: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, prune_kernel<MINI789>, kPruneThreads, 0); break;
     default: break;
   }
   return b > 0 ? b : 1;
