@@ -11,6 +11,8 @@ the 4 batches.  Weak scaling: rank r walks its own contiguous 2^24-start shard o
 global K0 stream.  Timing: CUDA events on the launching stream, barrier + synchronize on
 both sides, max over ranks; L2 is flushed (256 MiB write) before every step.  One NCCL
 all-reduce after the timed region gathers the chain-length histogram and edge counts.
+`--total-log2 30 --steps 256/N` is configs[3] (2^30 starts split over N ranks, strong
+scaling).
 
 `--impl reference` times the reference algorithm on the host cores instead (the C
 restatement in oracle/, since the Python reference cannot travel to the GPU box).
@@ -145,6 +147,8 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch-log2", type=int, default=22)
     ap.add_argument("--workload-log2", type=int, default=24)
+    ap.add_argument("--total-log2", type=int, default=0,
+                    help="strong scaling (configs[3]): 2^k starts in total, split over the ranks")
     ap.add_argument("--refill", type=int, default=0)
     ap.add_argument("--starts", default="k0", choices=["k0", "random"],
                     help="k0: special nodes (the metric's workload); random: uniform valid states")
@@ -192,6 +196,10 @@ def main() -> None:
     stream = torch.cuda.Stream(dev)  # explicit stream: kernels and events share it
     torch.cuda.set_stream(stream)
 
+    if args.total_log2:  # configs[3]: a fixed total split over the ranks
+        args.workload_log2 = args.total_log2 - (world.bit_length() - 1)
+        if 1 << args.total_log2 != world << args.workload_log2:
+            raise SystemExit("--total-log2 needs a power-of-two world size")
     per_gpu = 1 << args.workload_log2
     batch = 1 << args.batch_log2
     nbatches = max(1, per_gpu // batch)
@@ -329,13 +337,15 @@ def main() -> None:
         line = {
             "metric": METRIC, "value": value, "unit": "transitions/s", "edges_per_s": edges_per_s,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
+            "scaling": "strong" if args.total_log2 else "weak",
             "vs_baseline": value / PAPER_GTX580,
             "vs_baseline_ref": "paper GTX 580 bitsliced walk, 9,800 nodes/s x 11.17e6 clocks (PAPER.md:478-479)",
             "dtype": "u32 (bitsliced words, 32 lanes)",
             "data": "synthetic (" + ("K0 seeded special A5/1 nodes" if args.starts == "k0"
                                      else "seeded uniform random valid A5/1 states") + ")",
-            "config": {"workload": f"configs[1]: 2^{args.workload_log2} "
+            "config": {"workload": (f"configs[3]: 2^{args.total_log2} in total, " if args.total_log2 else "configs[1]: ")
+                                   + f"2^{args.workload_log2} "
                                    f"{'special A5/1 start nodes' if args.starts == 'k0' else 'uniform random A5/1 states'}"
                                    f" per GPU, walked {LEGS} hop(s) to the next special node, stride {STRIDE_}; "
                                    f"one step = one batch of 2^{args.batch_log2}", "starts_per_step_per_gpu": batch,
