@@ -261,7 +261,11 @@ __global__ void __launch_bounds__(256) enumerate_plane_kernel(uint64_t r2_lo, ui
                                                               uint64_t* __restrict__ d_count) {
   constexpr int CT1 = S::CT1;
   constexpr uint32_t kLowMask = (1u << CT1) - 1u;
-  constexpr int kU = 8;  // pairs per lane per iteration (a warp covers 512 slots)
+#ifndef LC_K2_PAIRS
+#define LC_K2_PAIRS 8
+#endif
+  constexpr int kU = LC_K2_PAIRS;  // pairs per lane per iteration (a warp covers 64 * kU slots)
+  constexpr int kSpan = (64 * kU + 255) / 256 + 1;  // runs a chunk can touch (A5/1 runs: 256)
   // work units: a row's virtual slots in equal pieces, so blocks get equal work whatever
   // the row's pattern count (1..4 runs per 2^(ct1+2) R1 values)
   constexpr uint64_t kRowSlots = 1ull << S::L1;  // >= any row's virtual slot count
@@ -306,12 +310,12 @@ __global__ void __launch_bounds__(256) enumerate_plane_kernel(uint64_t r2_lo, ui
     }
     for (uint64_t it = warp; it * (32 * kU) < npairs; it += nwarps) {
       const uint64_t vbase = v_first + it * (64 * kU);
-      uint32_t pre[3] = {0, 0, 0}, run0 = 0;
+      uint32_t pre[kSpan] = {}, run0 = 0;
       if constexpr (kFast) {  // the chunk spans runs run0 .. run0 + 2
         run0 = static_cast<uint32_t>(vbase >> CT1);
         uint32_t high = run0 / na, rank = run0 - high * na;
 #pragma unroll
-        for (int r = 0; r < 3; ++r) {
+        for (int r = 0; r < kSpan; ++r) {
           const uint32_t p = rank == 0 ? prank[0] : rank == 1 ? prank[1] : rank == 2 ? prank[2] : prank[3];
           pre[r] = (high << (CT1 + 2)) | (p << CT1);
           if (++rank == na) {
@@ -327,8 +331,12 @@ __global__ void __launch_bounds__(256) enumerate_plane_kernel(uint64_t r2_lo, ui
         uint64_t x0, x1;
         if constexpr (kFast) {
           const uint32_t d0 = static_cast<uint32_t>(v >> CT1) - run0, d1 = static_cast<uint32_t>((v + 1) >> CT1) - run0;
-          const uint32_t q0 = d0 == 0 ? pre[0] : d0 == 1 ? pre[1] : pre[2];
-          const uint32_t q1 = d1 == 0 ? pre[0] : d1 == 1 ? pre[1] : pre[2];
+          uint32_t q0 = pre[0], q1 = pre[0];
+#pragma unroll
+          for (int r = 1; r < kSpan; ++r) {
+            q0 = d0 == static_cast<uint32_t>(r) ? pre[r] : q0;
+            q1 = d1 == static_cast<uint32_t>(r) ? pre[r] : q1;
+          }
           x0 = row_bits | (q0 | (static_cast<uint32_t>(v) & kLowMask));
           x1 = row_bits | (q1 | (static_cast<uint32_t>(v + 1) & kLowMask));
         } else {
