@@ -449,25 +449,23 @@ __device__ __forceinline__ uint64_t child_of(uint64_t y, int q) {
 #define LC_PRUNE_THREADS 128
 #endif
 constexpr int kRing = LC_PRUNE_RING;
-constexpr int kPruneThreads = LC_PRUNE_THREADS;  // the ring takes kRing * 12 B per thread of shared memory
+constexpr int kPruneThreads = LC_PRUNE_THREADS;  // the ring takes kRing * 10 B per thread of shared memory
 constexpr int kTailBurst = 32;  // steps per warp vote once no candidate is left to take
 
 struct Ring {
-  uint32_t* lo;  // [kRing][kPruneThreads]: node low word
-  uint32_t* hi;  //                   node high word
-  uint32_t* dm;  //                   depth << 4 | remaining child mask
+  uint64_t* node;  // [kRing][kPruneThreads]: the branch node
+  uint16_t* dm;    //                         depth << 4 | remaining child mask
   uint32_t top, cnt;
   bool lost;
   __device__ __forceinline__ uint32_t at(uint32_t slot) const { return slot * kPruneThreads + threadIdx.x; }
   __device__ __forceinline__ void push(uint64_t y, uint64_t d, uint32_t mask) {
-    if (d >= (1ull << 27)) {  // depth does not fit the slot: leave it to the stackless climb
+    if (d >= (1ull << 12)) {  // depth does not fit the slot: leave it to the stackless climb
       lost = true;
       return;
     }
-    top = (top + 1) & (kRing - 1);
-    lo[at(top)] = static_cast<uint32_t>(y);
-    hi[at(top)] = static_cast<uint32_t>(y >> 32);
-    dm[at(top)] = (static_cast<uint32_t>(d) << 4) | mask;
+    top = top + 1 == static_cast<uint32_t>(kRing) ? 0u : top + 1;
+    node[at(top)] = y;
+    dm[at(top)] = static_cast<uint16_t>((static_cast<uint32_t>(d) << 4) | mask);
     if (cnt == kRing) lost = true;
     else ++cnt;
   }
@@ -549,15 +547,15 @@ __device__ __forceinline__ int prune_step(uint64_t& x, uint64_t& d, uint64_t& ac
   if (finished) {
     if (ring.cnt) {  // resume the deepest pending branch point
       const uint32_t slot = ring.at(ring.top);
-      src = static_cast<uint64_t>(ring.lo[slot]) | (static_cast<uint64_t>(ring.hi[slot]) << 32);
+      src = ring.node[slot];
       const uint32_t dm = ring.dm[slot];
       const uint32_t mask = dm & 15u;
       q = 31 - __clz(mask);
       const uint32_t rest = mask & ~(1u << q);
       if (rest) {
-        ring.dm[slot] = (dm & ~15u) | rest;
+        ring.dm[slot] = static_cast<uint16_t>((dm & ~15u) | rest);
       } else {
-        ring.top = (ring.top - 1) & (kRing - 1);
+        ring.top = ring.top == 0u ? kRing - 1 : ring.top - 1;
         --ring.cnt;
       }
       d = (dm >> 4) + 1;
@@ -582,11 +580,12 @@ __global__ void __launch_bounds__(kPruneThreads) prune_kernel(const uint64_t* __
                                                          uint8_t* __restrict__ removed,
                                                          uint64_t* __restrict__ work,
                                                          unsigned long long* queue) {
-  __shared__ uint32_t ring_lo[kRing * kPruneThreads], ring_hi[kRing * kPruneThreads], ring_dm[kRing * kPruneThreads];
+  __shared__ uint64_t ring_node[kRing * kPruneThreads];
+  __shared__ uint16_t ring_dm[kRing * kPruneThreads];
   const uint32_t lane = threadIdx.x & 31u;
   uint64_t i = 0, x = 0, d = 0, acc = 0;
   bool have = false, climb = false, drained = false;
-  Ring ring{ring_lo, ring_hi, ring_dm, 0, 0, false};
+  Ring ring{ring_node, ring_dm, 0, 0, false};
   for (;;) {
     if (!drained) {
       const uint32_t need = __ballot_sync(kFull, !have);
