@@ -22,6 +22,7 @@ from typing import Iterable, Iterator
 import numpy as np
 
 from . import _batch
+from . import _native as N
 from .bitslice import forward_to_candidate
 from .cipher import CandidateParams, CipherSpec, PredecessorTable, is_candidate, shared_table
 from .records import EdgeRecord
@@ -146,16 +147,38 @@ def _edges_chunk(args) -> list:
     return [(src, dest, dist) for src, (dest, dist) in zip(chunk, walked)]
 
 
+def _walk_sharded(sk: np.ndarray, params, spec, stride: int, devices: list):
+    """Contiguous shards walked concurrently, one host thread (and native context) per
+    device; results in input order."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    shards = np.array_split(sk, len(devices))
+
+    def run(i):
+        return _batch.walk(shards[i], params, spec, stride=stride, legs=1, device=devices[i])
+
+    with ThreadPoolExecutor(len(devices)) as ex:  # ctypes releases the GIL in lc_walk
+        parts = list(ex.map(run, range(len(devices))))
+    return (np.concatenate([r.dst[:, 0] for r in parts]), np.concatenate([r.dist[:, 0] for r in parts]))
+
+
 def build_skeleton_edges(skeleton: list, params: CandidateParams, spec: CipherSpec,
                          table: PredecessorTable | None = None, stride: int = 1,
-                         workers: int = 1) -> list:
+                         workers: int = 1, *, devices: list | None = None) -> list:
     """One weighted edge per skeleton node (pipeline.py:231-256); every destination
-    must be in the skeleton, else PruneSoundnessError."""
+    must be in the skeleton, else PruneSoundnessError.  ``workers`` (the reference's
+    process-pool size, pipeline.py:244-249) spreads contiguous shards over up to that
+    many GPUs of this process (or over ``devices``); the order is the input order."""
     sk = np.asarray(skeleton if isinstance(skeleton, np.ndarray) else list(skeleton), dtype=np.uint64)
     if sk.size == 0:
         raise ValueError("skeleton is empty")
-    res = _batch.walk(sk, params, spec, stride=stride, legs=1)
-    dst, dist = res.dst[:, 0], res.dist[:, 0]
+    if devices is None:
+        devices = list(range(max(1, min(int(workers), N.device_count()))))
+    if len(devices) > 1:
+        dst, dist = _walk_sharded(sk, params, spec, stride, devices)
+    else:
+        res = _batch.walk(sk, params, spec, stride=stride, legs=1, device=devices[0])
+        dst, dist = res.dst[:, 0], res.dist[:, 0]
     bad = _batch.first_missing(np.unique(sk), dst)
     if bad < sk.size:
         raise PruneSoundnessError(

@@ -158,3 +158,15 @@ def test_edges_chunk_worker(gpu, lc, specs, params):
     g = golden_npz("edges_mini789")
     rows = _edges_chunk((g["src"][:500].tolist(), params["mini789"], specs["mini789"], None, 1))
     assert rows == list(zip(g["src"][:500].tolist(), g["dst"][:500].tolist(), g["dist"][:500].tolist()))
+
+
+def test_build_skeleton_edges_sharded_devices(gpu, lc, specs, params):
+    """workers > 1: contiguous shards walked concurrently, one host thread and native
+    context per device (here twice the one GPU), results in input order."""
+    g = golden_npz("edges_mini789")
+    for devices in ([0, 0], [0, 0, 0]):
+        edges = lc.build_skeleton_edges(g["src"].tolist(), params["mini789"], specs["mini789"], devices=devices)
+        assert [e.destination for e in edges] == g["dst"].tolist()
+        assert [e.distance for e in edges] == g["dist"].tolist()
+    edges = lc.build_skeleton_edges(g["src"].tolist(), params["mini789"], specs["mini789"], workers=8)
+    assert [e.distance for e in edges] == g["dist"].tolist()
