@@ -152,12 +152,12 @@ def enumerate_rows(spec, params, r2_lo: int, r2_hi: int) -> np.ndarray:
         return out[: int(count.value)]
 
 
-def prune(cands, spec, params, mode: str, limit: int):
-    """Per-candidate (removed, work) of the step-2 prune (GPU stackless DFS)."""
+def prune(cands, spec, params, mode: str, limit: int, device=None):
+    """Per-candidate (removed, work) of the step-2 prune (GPU reverse DFS)."""
     c = _u64(cands)
     removed = np.zeros(c.size, dtype=np.uint8)
     work = np.zeros(c.size, dtype=np.uint64)
-    ctx = N.context()
+    ctx = N.context(device)
     rc = N.lib.lc_prune(ctx.handle, C.byref(N.spec_struct(spec)), params.fixed_r3, 0 if mode == "dfs" else 1,
                         int(limit), N.u64p(c), c.size, N.u8p(removed), N.u64p(work))
     if rc != N.LC_OK:

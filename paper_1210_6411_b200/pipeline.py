@@ -44,8 +44,8 @@ class PruneSoundnessError(RuntimeError):
 
 @dataclass(frozen=True)
 class PruneConfig:
-    """Bounded reverse traversal settings (pipeline.py:50-84).  ``workers`` is accepted
-    for API compatibility; the GPU kernel does not use host workers."""
+    """Bounded reverse traversal settings (pipeline.py:50-84).  ``workers`` (the
+    reference's process-pool size) is the number of GPUs the prune may spread over."""
 
     mode: str = "dfs"
     depth_limit: int | None = None
@@ -117,18 +117,33 @@ def enumerate_candidates(spec: CipherSpec, params: CandidateParams,
 
 def prune_shallow_segments(candidates: Iterable[int], config: PruneConfig, spec: CipherSpec,
                            params: CandidateParams,
-                           table: PredecessorTable | None = None) -> tuple:
+                           table: PredecessorTable | None = None, *, devices: list | None = None) -> tuple:
     """Drop candidates rooting shallow segments; survivors keep input order
-    (pipeline.py:192-222)."""
+    (pipeline.py:192-222).  ``config.workers`` (the reference's process-pool size) spreads
+    contiguous chunks over up to that many GPUs of this process (or over ``devices``)."""
     config.validate(spec)
     limit = config.depth_limit if config.mode == "dfs" else config.node_limit
     stats = PruneStats(mode=config.mode, limit=limit)
     cands = np.asarray(candidates if isinstance(candidates, np.ndarray) else list(candidates),
                        dtype=np.uint64)
+    if devices is None:
+        devices = list(range(max(1, min(int(config.workers), N.device_count()))))
+    chunks = [cands[lo: lo + _PRUNE_CHUNK_GPU] for lo in range(0, cands.size, _PRUNE_CHUNK_GPU)]
+    if len(devices) > 1 and len(chunks) == 1 and cands.size >= 2 * len(devices):
+        chunks = np.array_split(cands, len(devices))
+
+    def run(i):
+        return _batch.prune(chunks[i], spec, params, config.mode, limit, device=devices[i % len(devices)])
+
+    if len(devices) > 1 and len(chunks) > 1:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(len(devices)) as ex:  # one thread (and context) per device
+            results = list(ex.map(run, range(len(chunks))))
+    else:
+        results = [run(i) for i in range(len(chunks))]
     survivors = []
-    for lo in range(0, cands.size, _PRUNE_CHUNK_GPU):
-        chunk = cands[lo: lo + _PRUNE_CHUNK_GPU]
-        removed, work = _batch.prune(chunk, spec, params, config.mode, limit)
+    for chunk, (removed, work) in zip(chunks, results):
         survivors.append(chunk[~removed])
         stats.total += chunk.size
         stats.removed += int(removed.sum())

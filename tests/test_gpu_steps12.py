@@ -170,3 +170,17 @@ def test_build_skeleton_edges_sharded_devices(gpu, lc, specs, params):
         assert [e.distance for e in edges] == g["dist"].tolist()
     edges = lc.build_skeleton_edges(g["src"].tolist(), params["mini789"], specs["mini789"], workers=8)
     assert [e.distance for e in edges] == g["dist"].tolist()
+
+
+def test_prune_sharded_devices(gpu, lc, specs, params):
+    """config.workers / devices > 1: chunks pruned concurrently, survivors in input order,
+    statistics summed -- equal to the single-device result and the reference's."""
+    fx = golden_json("prune.json")
+    cands = fx["a51_cands"]
+    key = next(k for k in fx if k.startswith("a51_dfs_"))
+    want = fx[key]
+    cfg = lc.PruneConfig(mode="dfs", depth_limit=int(key.split("_")[2]))
+    for devices in ([0, 0], [0, 0, 0]):
+        surv, st = lc.prune_shallow_segments(cands, cfg, specs["a51"], params["a51"], devices=devices)
+        assert surv == want["survivors"]
+        assert (st.total, st.removed, st.expanded) == (want["total"], want["removed"], want["expanded"])
