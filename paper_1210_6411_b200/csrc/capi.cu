@@ -116,7 +116,7 @@ struct lc_ctx {
   int device = 0;
   int sms = 0;
   cudaStream_t stream = nullptr;
-  DevBuf meta, queue, stats, a, b, c, d, scratch, smmap, pq, pool_a, pool_b, need3;
+  DevBuf meta, queue, stats, a, b, c, d, scratch, smmap, pq, pool_a, pool_b, need3, spill;
   int mapped_sms = -1;  // SMs found by the %smid probe (-1: not probed yet)
   int need3_id = -1;    // spec / fixed R3 the need3 table was built for
   uint64_t need3_f = 0;
@@ -211,7 +211,7 @@ int lc_ctx_destroy(lc_ctx* ctx) {
   if (!ctx) return LC_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  for (DevBuf* b : {&ctx->meta, &ctx->queue, &ctx->stats, &ctx->a, &ctx->b, &ctx->c, &ctx->d, &ctx->scratch, &ctx->smmap, &ctx->pq, &ctx->pool_a, &ctx->pool_b, &ctx->need3})
+  for (DevBuf* b : {&ctx->meta, &ctx->queue, &ctx->stats, &ctx->a, &ctx->b, &ctx->c, &ctx->d, &ctx->scratch, &ctx->smmap, &ctx->pq, &ctx->pool_a, &ctx->pool_b, &ctx->need3, &ctx->spill})
     b->release();
   cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -633,8 +633,13 @@ int lc_prune_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int32_t
   LC_CUDA(ctx->pq.ensure(8));
   LC_CUDA(cudaMemsetAsync(ctx->pq.p, 0, 8, st));
   const int blocks = lc::prune_blocks_per_sm(id) * ctx->sms;
+#ifndef LC_PRUNE_SPILL
+#define LC_PRUNE_SPILL 512
+#endif
+  constexpr uint32_t kSpillCap = LC_PRUNE_SPILL;  // overflow entries per lane behind the shared-memory ring
+  LC_CUDA(ctx->spill.ensure(lc::prune_spill_bytes(blocks, kSpillCap)));
   LC_CUDA(lc::launch_prune(id, static_cast<uint32_t>(fixed_r3), mode, limit, d_cands, n, d_removed, d_work,
-                           ctx->pq.as<unsigned long long>(), blocks, st));
+                           ctx->pq.as<unsigned long long>(), ctx->spill.p, kSpillCap, blocks, st));
   g_launches += 1;
   return LC_OK;
 }

@@ -455,7 +455,9 @@ constexpr int kTailBurst = 32;  // steps per warp vote once no candidate is left
 struct Ring {
   uint64_t* node;  // [kRing][kPruneThreads]: the branch node
   uint16_t* dm;    //                         depth << 4 | remaining child mask
-  uint32_t top, cnt;
+  uint64_t* snode; // this lane's spill ring in global memory (older entries), [scap]
+  uint16_t* sdm;
+  uint32_t top, cnt, scnt, scap, sbase;  // spill entry k (0 = oldest) at (sbase + k) mod scap
   bool lost;
   __device__ __forceinline__ uint32_t at(uint32_t slot) const { return slot * kPruneThreads + threadIdx.x; }
   __device__ __forceinline__ void push(uint64_t y, uint64_t d, uint32_t mask) {
@@ -463,11 +465,27 @@ struct Ring {
       lost = true;
       return;
     }
-    top = top + 1 == static_cast<uint32_t>(kRing) ? 0u : top + 1;
+    const uint32_t next = top + 1 == static_cast<uint32_t>(kRing) ? 0u : top + 1;
+    if (cnt == kRing) {  // full: the oldest entry (about to be overwritten) moves to the spill ring
+      if (scap) {
+        if (scnt == scap) {  // spill full too: drop its oldest entry (the climb recovers it)
+          sbase = sbase + 1 == scap ? 0u : sbase + 1;
+          --scnt;
+          lost = true;
+        }
+        const uint32_t k = sbase + scnt < scap ? sbase + scnt : sbase + scnt - scap;
+        snode[k] = node[at(next)];
+        sdm[k] = dm[at(next)];
+        ++scnt;
+      } else {
+        lost = true;
+      }
+    } else {
+      ++cnt;
+    }
+    top = next;
     node[at(top)] = y;
     dm[at(top)] = static_cast<uint16_t>((static_cast<uint32_t>(d) << 4) | mask);
-    if (cnt == kRing) lost = true;
-    else ++cnt;
   }
 };
 
@@ -545,6 +563,15 @@ __device__ __forceinline__ int prune_step(uint64_t& x, uint64_t& d, uint64_t& ac
     }
   }
   if (finished) {
+    if (ring.cnt == 0u && ring.scnt) {  // the ring ran dry: bring back the newest spilled entry
+      const uint32_t j = ring.sbase + ring.scnt - 1u;
+      const uint32_t k = j < ring.scap ? j : j - ring.scap;
+      ring.top = ring.top + 1 == static_cast<uint32_t>(kRing) ? 0u : ring.top + 1;
+      ring.node[ring.at(ring.top)] = ring.snode[k];
+      ring.dm[ring.at(ring.top)] = ring.sdm[k];
+      ring.cnt = 1;
+      --ring.scnt;
+    }
     if (ring.cnt) {  // resume the deepest pending branch point
       const uint32_t slot = ring.at(ring.top);
       src = ring.node[slot];
@@ -579,13 +606,16 @@ __global__ void __launch_bounds__(kPruneThreads) prune_kernel(const uint64_t* __
                                                          uint32_t F, int mode, uint64_t limit,
                                                          uint8_t* __restrict__ removed,
                                                          uint64_t* __restrict__ work,
-                                                         unsigned long long* queue) {
+                                                         unsigned long long* queue, uint64_t* spill_node,
+                                                         uint16_t* spill_dm, uint32_t spill_cap) {
   __shared__ uint64_t ring_node[kRing * kPruneThreads];
   __shared__ uint16_t ring_dm[kRing * kPruneThreads];
   const uint32_t lane = threadIdx.x & 31u;
   uint64_t i = 0, x = 0, d = 0, acc = 0;
   bool have = false, climb = false, drained = false;
-  Ring ring{ring_node, ring_dm, 0, 0, false};
+  const uint64_t gtid = blockIdx.x * static_cast<uint64_t>(kPruneThreads) + threadIdx.x;
+  Ring ring{ring_node, ring_dm, spill_node ? spill_node + gtid * spill_cap : nullptr,
+            spill_dm ? spill_dm + gtid * spill_cap : nullptr, 0, 0, 0, spill_node ? spill_cap : 0u, 0, false};
   for (;;) {
     if (!drained) {
       const uint32_t need = __ballot_sync(kFull, !have);
@@ -604,6 +634,8 @@ __global__ void __launch_bounds__(kPruneThreads) prune_kernel(const uint64_t* __
             climb = false;
             have = true;
             ring.cnt = 0;
+            ring.scnt = 0;
+            ring.sbase = 0;
             ring.lost = false;
           }
         }
@@ -699,11 +731,19 @@ cudaError_t launch_random_candidates(SpecId id, uint32_t F, uint64_t seed, uint6
   });
 }
 
+uint64_t prune_spill_bytes(int blocks, uint32_t cap) {
+  return static_cast<uint64_t>(blocks) * kPruneThreads * cap * (8 + 2) + 512;
+}
+
 cudaError_t launch_prune(SpecId id, uint32_t F, int mode, uint64_t limit, const uint64_t* cands,
                          uint64_t n, uint8_t* removed, uint64_t* work, unsigned long long* queue,
-                         int blocks, cudaStream_t stream) {
+                         void* spill, uint32_t spill_cap, int blocks, cudaStream_t stream) {
+  uint64_t* spill_node = spill ? static_cast<uint64_t*>(spill) : nullptr;
+  uint16_t* spill_dm =
+      spill ? reinterpret_cast<uint16_t*>(spill_node + static_cast<uint64_t>(blocks) * kPruneThreads * spill_cap)
+            : nullptr;
   LC_DISPATCH(id, prune_kernel<S><<<blocks, kPruneThreads, 0, stream>>>(cands, n, F, mode, limit, removed, work,
-                                                                   queue);
+                                                                   queue, spill_node, spill_dm, spill_cap);
               return cudaGetLastError());
 }
 

@@ -100,9 +100,12 @@ cudaError_t launch_random_candidates(SpecId id, uint32_t F, uint64_t seed, uint6
                                      cudaStream_t stream, int* launches);
 uint64_t random_scratch_words(uint64_t trials);
 
+// spill: per-lane global overflow stacks behind the shared-memory ring (spill_cap
+// entries per lane, prune_spill_bytes(blocks, spill_cap) bytes; null: none).
+uint64_t prune_spill_bytes(int blocks, uint32_t cap);
 cudaError_t launch_prune(SpecId id, uint32_t F, int mode, uint64_t limit, const uint64_t* cands,
-                         uint64_t n, uint8_t* removed, uint64_t* work,
-                         unsigned long long* queue, int blocks, cudaStream_t stream);
+                         uint64_t n, uint8_t* removed, uint64_t* work, unsigned long long* queue,
+                         void* spill, uint32_t spill_cap, int blocks, cudaStream_t stream);
 int prune_blocks_per_sm(SpecId id);
 
 cudaError_t measure_lop3_peak(int sms, double* ops_per_s, double* sm_mhz);
