@@ -451,6 +451,10 @@ __device__ __forceinline__ uint64_t child_of(uint64_t y, int q) {
 constexpr int kRing = LC_PRUNE_RING;
 constexpr int kPruneThreads = LC_PRUNE_THREADS;  // the ring takes kRing * 10 B per thread of shared memory
 constexpr int kTailBurst = 32;  // steps per warp vote once no candidate is left to take
+#ifndef LC_PRUNE_BULK_BURST
+#define LC_PRUNE_BULK_BURST 4
+#endif
+constexpr int kBulkBurst = LC_PRUNE_BULK_BURST;  // steps per warp vote while candidates remain
 
 struct Ring {
   uint64_t* node;  // [kRing][kPruneThreads]: the branch node
@@ -646,10 +650,9 @@ __global__ void __launch_bounds__(kPruneThreads) prune_kernel(const uint64_t* __
       // once the candidates are drained nothing can be refilled: run bursts of steps
       // between warp votes (the tail is latency-bound on the longest traversals)
       int r = prune_step<S>(x, d, acc, climb, ring, F, mode, limit);
-      if (drained) {
+      const int burst = drained ? kTailBurst : kBulkBurst;
 #pragma unroll 1
-        for (int k = 1; k < kTailBurst && r == 0; ++k) r = prune_step<S>(x, d, acc, climb, ring, F, mode, limit);
-      }
+      for (int k = 1; k < burst && r == 0; ++k) r = prune_step<S>(x, d, acc, climb, ring, F, mode, limit);
       if (r != 0) {
         removed[i] = r == 1 ? 1 : 0;
         work[i] = acc;
