@@ -359,26 +359,13 @@ __global__ void __launch_bounds__(256) enumerate_plane_kernel(uint64_t r2_lo, ui
 }
 
 // ---------------------------------------------------------------- K3: step-2 prune
-// Thread per candidate, stackless depth-first traversal of the candidate's segment (the
-// reverse tree through predecessors that are not candidates, pipeline.py:121-129).  The
-// pop order of the reference's LIFO stack (pipeline.py:132-144) is a preorder that visits
-// children in reverse LUT order; it is replayed without a stack by returning to the
-// parent with one forward clock and moving to the next-lower sibling, so the
-// order-dependent `expanded` counter matches exactly.  BFS mode (pipeline.py:147-160)
-// only needs the segment size capped at node_limit + 1, which is order-independent.
-
-// Child q of node y (pattern kClockPatterns[q]) from y's registers and their unsteps.
-template <class S>
-struct Node {
-  uint32_t r1, r2, r3, u1, u2, u3;
-  uint32_t mask;  // bit q: pattern q yields a valid, non-candidate predecessor
-  __device__ __forceinline__ uint64_t child(int q) const {
-    const int p = clock_pattern(q & 3);
-    const uint32_t p1 = (p & 1) ? u1 : r1, p2 = (p & 2) ? u2 : r2, p3 = (p & 4) ? u3 : r3;
-    return static_cast<uint64_t>(p1) | (static_cast<uint64_t>(p2) << S::O2) |
-           (static_cast<uint64_t>(p3) << S::O3);
-  }
-};
+// Thread per candidate, depth-first traversal of the candidate's segment (the reverse
+// tree through predecessors that are not candidates, pipeline.py:121-129).  The pop
+// order of the reference's LIFO stack (pipeline.py:132-144) is a preorder that visits
+// children in reverse LUT order; it is replayed with a per-lane ring of pending branch
+// points (shared memory, spilling to global memory), so the order-dependent `expanded`
+// counter matches exactly.  BFS mode (pipeline.py:147-160) only needs the segment size
+// capped at node_limit + 1, which is order-independent.
 
 // The predecessor table as 64 nibbles (bit q of nibble idx = pattern q consistent at
 // table index idx), packed in four 64-bit immediates.
@@ -397,34 +384,8 @@ __device__ __forceinline__ uint32_t pattern_set(uint32_t idx) {
   return static_cast<uint32_t>(w >> ((idx & 15u) << 2)) & 15u;
 }
 
-// Children of y in the segment: y's predecessors (cipher.py:342-369) minus special
-// nodes (pipeline.py:121-129).  Two facts keep this short: predecessors of a valid state
-// never have a zero register (unstep is a bijection fixing 0), and a child c's successor
-// is y itself, so is_candidate(c) (cipher.py:420-428) = R3(c) == F && R3(y) != F &&
-// preds(c) != {} -- only patterns that unstep R3 can land on the plane, and only when
-// unstep(R3(y)) == F (then R3(y) != F automatically); that rare case pays for the
-// children's table lookups.
-template <class S>
-__device__ __forceinline__ Node<S> expand_node(uint64_t y, uint32_t F) {
-  Node<S> nd;
-  nd.r1 = static_cast<uint32_t>(y & S::M1);
-  nd.r2 = static_cast<uint32_t>((y >> S::O2) & S::M2);
-  nd.r3 = static_cast<uint32_t>((y >> S::O3) & S::M3);
-  nd.u1 = unstep<S::L1, S::T1>(nd.r1);
-  nd.u2 = unstep<S::L2, S::T2>(nd.r2);
-  nd.u3 = unstep<S::L3, S::T3>(nd.r3);
-  uint32_t m = pattern_set(table_index<S>(y));
-  if (nd.u3 == F) {
-#pragma unroll
-    for (int q = 1; q < 4; ++q)
-      if (((m >> q) & 1u) && ((kNonEmpty >> table_index<S>(nd.child(q))) & 1ull)) m &= ~(1u << q);
-  }
-  nd.mask = m;
-  return nd;
-}
-
-// Child q of the node y (its registers unstepped on demand): used when resuming a
-// pending branch point.
+// Child q of the node y: y's predecessor under clock pattern CLOCK_PATTERNS[q], the
+// registers of the pattern unstepped (cipher.py:342-369).
 template <class S>
 __device__ __forceinline__ uint64_t child_of(uint64_t y, int q) {
   const uint32_t r1 = static_cast<uint32_t>(y & S::M1), r2 = static_cast<uint32_t>((y >> S::O2) & S::M2),
@@ -493,8 +454,13 @@ struct Ring {
   }
 };
 
-// The child mask of x alone (expand_node without building the children): the table
-// entry, minus the rare special-node children (only when unstep(R3(x)) == F).
+// Children of x in the segment, as a pattern mask: x's predecessors (cipher.py:342-369)
+// minus special nodes (pipeline.py:121-129).  Two facts keep this short: predecessors of
+// a valid state never have a zero register (unstep is a bijection fixing 0), and a child
+// c's successor is x itself, so is_candidate(c) (cipher.py:420-428) = R3(c) == F &&
+// R3(x) != F && preds(c) != {} -- only patterns that unstep R3 can land on the plane, and
+// only when unstep(R3(x)) == F (then R3(x) != F automatically); that rare case pays for
+// the children's table lookups.
 template <class S>
 __device__ __forceinline__ uint32_t child_mask(uint64_t x, uint32_t F) {
   uint32_t m = pattern_set(table_index<S>(x));
