@@ -169,6 +169,13 @@ int lc_first_missing(lc_ctx *ctx, const uint64_t *sorted_set, uint64_t m, const 
 int lc_sort_edges(lc_ctx *ctx, uint64_t n, uint64_t *src, uint64_t *dst, uint64_t *dist,
                   uint64_t *subtree_size, uint64_t *subtree_depth);
 
+/* Edge-output writer: 40-byte little-endian '<5Q' records (records.py:24-36) from
+ * device columns, d_out = 5 * n u64 words (subtree_size / subtree_depth may be NULL:
+ * zero).  Enqueued on `stream`. */
+int lc_pack_records_device(lc_ctx *ctx, uint64_t n, const uint64_t *d_src, const uint64_t *d_dst,
+                           const uint64_t *d_dist, const uint64_t *d_subtree_size,
+                           const uint64_t *d_subtree_depth, uint64_t *d_out, void *stream);
+
 /* Replaces reduce.cut_leaves_pass (reduce.py:118-186; max_passes = 1) and
  * cut_leaves_to_fixpoint (reduce.py:189-223; max_passes = 0) on records held in host
  * buffers (SoA, sorted by unique source), in place: the first *n_out records are the

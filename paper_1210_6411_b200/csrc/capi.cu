@@ -730,6 +730,19 @@ int lc_sort_edges(lc_ctx* ctx, uint64_t n, uint64_t* src, uint64_t* dst, uint64_
   return LC_OK;
 }
 
+int lc_pack_records_device(lc_ctx* ctx, uint64_t n, const uint64_t* d_src, const uint64_t* d_dst,
+                           const uint64_t* d_dist, const uint64_t* d_subtree_size, const uint64_t* d_subtree_depth,
+                           uint64_t* d_out, void* stream) {
+  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  if (n && (!d_src || !d_dst || !d_dist || !d_out)) return fail(LC_ERR_ARG, "null buffer");
+  LC_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  int launches = 0;
+  LC_CUDA(lc::pack_records_device(n, d_src, d_dst, d_dist, d_subtree_size, d_subtree_depth, d_out, st, &launches));
+  g_launches += launches;
+  return LC_OK;
+}
+
 int lc_cut_leaves(lc_ctx* ctx, uint64_t n, uint64_t* src, uint64_t* dst, uint64_t* dist, uint64_t* subtree_size,
                   uint64_t* subtree_depth, uint32_t max_passes, uint64_t* pass_stats, uint32_t max_stats,
                   uint32_t* n_passes, uint64_t* n_out) {

@@ -175,6 +175,9 @@ cudaError_t count_cycles_device(uint64_t n, const uint64_t* src, const uint64_t*
                                 const uint64_t* size, uint64_t* leader, uint64_t* hops_out, uint64_t* clocks_out,
                                 uint64_t* tree_out, uint64_t* n_cycles, unsigned int* err_out, void* scratch,
                                 cudaStream_t st, int* launches);
+cudaError_t pack_records_device(uint64_t n, const uint64_t* src, const uint64_t* dst, const uint64_t* dist,
+                                const uint64_t* size, const uint64_t* depth, uint64_t* out, cudaStream_t st,
+                                int* launches);
 size_t sort_scratch_bytes(uint64_t n);
 cudaError_t sort_records_device(uint64_t n, uint64_t* const* cols, int ncols, void* scratch, size_t scratch_bytes,
                                 cudaStream_t st, int* launches);

@@ -765,6 +765,28 @@ cudaError_t count_cycles_device(uint64_t n, const uint64_t* src, const uint64_t*
   return cudaSuccess;
 }
 
+// 40-byte '<5Q' edge records (records.py:24-36) from SoA columns: out[5i + k] = col_k[i]
+// (size/depth may be null: zero).  One thread per output word, so the stores are
+// coalesced and the column reads are five interleaved streams.
+__global__ void pack_records_kernel(uint64_t n, const uint64_t* __restrict__ c0, const uint64_t* __restrict__ c1,
+                                    const uint64_t* __restrict__ c2, const uint64_t* __restrict__ c3,
+                                    const uint64_t* __restrict__ c4, uint64_t* __restrict__ out) {
+  GRID_STRIDE(w, 5 * n) {
+    const uint64_t i = w / 5, k = w - 5 * i;
+    const uint64_t* c = k == 0 ? c0 : k == 1 ? c1 : k == 2 ? c2 : k == 3 ? c3 : c4;
+    out[w] = c ? c[i] : 0ull;
+  }
+}
+
+cudaError_t pack_records_device(uint64_t n, const uint64_t* src, const uint64_t* dst, const uint64_t* dist,
+                                const uint64_t* size, const uint64_t* depth, uint64_t* out, cudaStream_t st,
+                                int* launches) {
+  if (n == 0) return cudaSuccess;
+  pack_records_kernel<<<grid_for(5 * n), kT, 0, st>>>(n, src, dst, dist, size, depth, out);
+  ++*launches;
+  return cudaGetLastError();
+}
+
 // Edge-output stage: records sorted ascending by source, the
 // precondition of the edge file format and of step 4 (records.py:3-5, reduce.py:3-4).
 // LSD radix sort of (source, row) pairs (CUB), then a gather of the other columns.

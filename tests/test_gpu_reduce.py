@@ -110,3 +110,22 @@ def test_reduce_errors(gpu, lc, tmp_path):
         lc.count_cycles([lc.EdgeRecord(1, 2, 1, 0, 0), lc.EdgeRecord(1, 2, 1, 0, 0)])
     with pytest.raises(ValueError):
         lc.cut_leaves_pass(tmp_path / "x.bin", tmp_path / "y.bin", lc.ReduceConfig(memory_budget=1024))
+
+
+def test_write_edge_tensors_byte_identical(gpu, tmp_path):
+    """GPU record packer (lc_pack_records_device) == the reference's write_edges bytes."""
+    import torch
+
+    from paper_1210_6411_b200.records import EdgeRecord, write_edge_tensors, write_edges
+
+    rng = np.random.default_rng(5)
+    cols = [rng.integers(0, 1 << 63, size=1000, dtype=np.int64).astype(np.uint64) for _ in range(5)]
+    write_edges(tmp_path / "a.bin", [EdgeRecord(*map(int, r)) for r in zip(*cols)])
+    t = [torch.from_numpy(c.view(np.int64)).cuda() for c in cols]
+    write_edge_tensors(tmp_path / "b.bin", *t)
+    assert (tmp_path / "a.bin").read_bytes() == (tmp_path / "b.bin").read_bytes()
+    write_edges(tmp_path / "c.bin", [EdgeRecord(int(s), int(d), int(w), 0, 0) for s, d, w in zip(*cols[:3])])
+    write_edge_tensors(tmp_path / "d.bin", *t[:3])
+    assert (tmp_path / "c.bin").read_bytes() == (tmp_path / "d.bin").read_bytes()
+    write_edge_tensors(tmp_path / "e.bin", *(x[:0] for x in t[:3]))
+    assert (tmp_path / "e.bin").read_bytes() == b""
