@@ -411,6 +411,7 @@ __device__ __forceinline__ uint64_t child_of(uint64_t y, int q) {
 #endif
 constexpr int kRing = LC_PRUNE_RING;
 constexpr int kPruneThreads = LC_PRUNE_THREADS;  // the ring takes kRing * 10 B per thread of shared memory
+constexpr uint64_t kDepthCap = 1u << 12;  // ring entries hold depths below this (12-bit field)
 constexpr int kTailBurst = 32;  // steps per warp vote once no candidate is left to take
 #ifndef LC_PRUNE_BULK_BURST
 #define LC_PRUNE_BULK_BURST 4
@@ -426,10 +427,7 @@ struct Ring {
   bool lost;
   __device__ __forceinline__ uint32_t at(uint32_t slot) const { return slot * kPruneThreads + threadIdx.x; }
   __device__ __forceinline__ void push(uint64_t y, uint64_t d, uint32_t mask) {
-    if (d >= (1ull << 12)) {  // depth does not fit the slot: leave it to the stackless climb
-      lost = true;
-      return;
-    }
+    if (d >= kDepthCap) return;  // no room for the depth: found again by climbing (see prune_step)
     const uint32_t next = top + 1 == static_cast<uint32_t>(kRing) ? 0u : top + 1;
     if (cnt == kRing) {  // full: the oldest entry (about to be overwritten) moves to the spill ring
       if (scap) {
@@ -533,6 +531,10 @@ __device__ __forceinline__ int prune_step(uint64_t& x, uint64_t& d, uint64_t& ac
     }
   }
   if (finished) {
+    if (d > kDepthCap) {  // x's parent sits at depth >= kDepthCap, which the ring cannot hold:
+      climb = true;       // look for x's lower siblings by climbing (entries above are in the ring)
+      return 0;
+    }
     if (ring.cnt == 0u && ring.scnt) {  // the ring ran dry: bring back the newest spilled entry
       const uint32_t j = ring.sbase + ring.scnt - 1u;
       const uint32_t k = j < ring.scap ? j : j - ring.scap;

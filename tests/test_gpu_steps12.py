@@ -184,3 +184,18 @@ def test_prune_sharded_devices(gpu, lc, specs, params):
         surv, st = lc.prune_shallow_segments(cands, cfg, specs["a51"], params["a51"], devices=devices)
         assert surv == want["survivors"]
         assert (st.total, st.removed, st.expanded) == (want["total"], want["removed"], want["expanded"])
+
+
+def test_prune_deep_limit_matches_oracle(gpu, lc, specs, params):
+    """Depth limits beyond the ring's 12-bit depth field (>= 4096) take the stackless-climb
+    fallback for the deep part of a traversal; results and the LIFO `expanded` counter
+    still equal the C restatement (oracle/lfsr_oracle.c, pinned to the reference)."""
+    from oracle import port
+    from paper_1210_6411_b200 import _batch
+
+    cands = lc.random_candidates_gpu(specs["a51"], params["a51"], seed=77, n=512)
+    for limit in (4095, 4097, 6000):
+        removed, work = _batch.prune(cands, specs["a51"], params["a51"], "dfs", limit)
+        o_removed, o_work = port.prune(specs["a51"], 0x2AAA00, "dfs", limit, cands)
+        assert (removed == np.asarray(o_removed).astype(bool)).all(), limit
+        assert (work == np.asarray(o_work)).all(), limit
