@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -636,10 +637,14 @@ int lc_prune_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int32_t
 #ifndef LC_PRUNE_SPILL
 #define LC_PRUNE_SPILL 512
 #endif
-  constexpr uint32_t kSpillCap = LC_PRUNE_SPILL;  // overflow entries per lane behind the shared-memory ring
-  LC_CUDA(ctx->spill.ensure(lc::prune_spill_bytes(blocks, kSpillCap)));
+  // overflow entries per lane behind the shared-memory ring; LFSR_PRUNE_SPILL overrides it
+  // (testing: small values exercise the drop-and-climb fallback)
+  uint32_t spill_cap = LC_PRUNE_SPILL;
+  if (const char* env = getenv("LFSR_PRUNE_SPILL")) spill_cap = static_cast<uint32_t>(strtoul(env, nullptr, 10));
+  if (spill_cap) LC_CUDA(ctx->spill.ensure(lc::prune_spill_bytes(blocks, spill_cap)));
   LC_CUDA(lc::launch_prune(id, static_cast<uint32_t>(fixed_r3), mode, limit, d_cands, n, d_removed, d_work,
-                           ctx->pq.as<unsigned long long>(), ctx->spill.p, kSpillCap, blocks, st));
+                           ctx->pq.as<unsigned long long>(), spill_cap ? ctx->spill.p : nullptr, spill_cap, blocks,
+                           st));
   g_launches += 1;
   return LC_OK;
 }

@@ -199,3 +199,47 @@ def test_prune_deep_limit_matches_oracle(gpu, lc, specs, params):
         o_removed, o_work = port.prune(specs["a51"], 0x2AAA00, "dfs", limit, cands)
         assert (removed == np.asarray(o_removed).astype(bool)).all(), limit
         assert (work == np.asarray(o_work)).all(), limit
+
+
+@pytest.mark.parametrize("spill", ["0", "1", "3"])
+def test_prune_small_spill_matches_reference(gpu, lc, specs, params, spill):
+    """Tiny (or no) global spill behind the 32-entry ring forces the drop-oldest +
+    stackless-climb fallback on deep traversals; survivors and the per-candidate LIFO
+    `expanded` counters must still equal the reference's (prune.json) and the C
+    restatement.  The kernel reads LFSR_PRUNE_SPILL at launch, so it runs in a child
+    process."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = r'''
+import json, numpy as np, sys
+sys.path.insert(0, ".")
+sys.path.insert(0, "tests")
+import paper_1210_6411_b200 as lc
+from paper_1210_6411_b200 import _batch
+from conftest import golden_json
+from oracle import port
+fx = golden_json("prune.json")
+cands = fx["a51_cands"]
+p = lc.CandidateParams.from_spec(lc.A51, 0x2AAA00)
+ok = True
+for key, want in fx.items():
+    if not key.startswith("a51_") or key == "a51_cands":
+        continue
+    _, mode, lim = key.split("_")
+    removed, work = _batch.prune(cands, lc.A51, p, mode, int(lim))
+    surv = [c for c, r in zip(cands, removed) if not r]
+    ok = ok and surv == want["survivors"] and int(work.sum()) == want["expanded"]
+extra = lc.random_candidates_gpu(lc.A51, p, seed=5, n=256)
+removed, work = _batch.prune(extra, lc.A51, p, "dfs", 6000)
+o_removed, o_work = port.prune(lc.A51, 0x2AAA00, "dfs", 6000, extra)
+ok = ok and (removed == np.asarray(o_removed).astype(bool)).all() and (work == np.asarray(o_work)).all()
+print(json.dumps({"ok": bool(ok)}))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LFSR_PRUNE_SPILL=spill)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert json.loads(r.stdout.strip().splitlines()[-1])["ok"]
