@@ -243,3 +243,21 @@ print(json.dumps({"ok": bool(ok)}))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert json.loads(r.stdout.strip().splitlines()[-1])["ok"]
+
+
+def test_enumerate_overflow_returns_prefix(gpu, lc, specs, params):
+    """lc_enumerate with too small a buffer: LC_ERR_OVERFLOW, the full count, and the
+    ascending prefix that fits (the writer's cap check on its 16-byte pair stores)."""
+    import ctypes as C
+
+    from paper_1210_6411_b200 import _native as N
+
+    full = lc.enumerate_candidates_array(specs["a51"], params["a51"], 0x1234, 0x1236)
+    ctx = N.context()
+    for cap in (1, 2, 3, 1000, 1001, full.size - 1):
+        out = np.zeros(cap, dtype=np.uint64)
+        count = C.c_uint64(0)
+        rc = N.lib.lc_enumerate(ctx.handle, C.byref(N.spec_struct(specs["a51"])), params["a51"].fixed_r3, 0x1234,
+                                0x1236, N.u64p(out), cap, C.byref(count))
+        assert rc == N.LC_ERR_OVERFLOW and count.value == full.size
+        assert (out == full[:cap]).all(), cap
