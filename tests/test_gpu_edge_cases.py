@@ -54,3 +54,26 @@ def test_cut_leaves_arrays_empty(gpu, lc):
     assert out[5] == [(0, 0, 0)] and all(c.size == 0 for c in out[:5])
     out = lc.cut_leaves_arrays(z, z, z, z, z, max_passes=1)
     assert out[5] == [(0, 0, 0)]
+
+
+def test_minimal_walk_sort_and_generator_inputs(gpu, lc, specs, params):
+    from paper_1210_6411_b200 import _batch
+
+    prm, spec = params["a51"], specs["a51"]
+    assert lc.random_candidates_gpu(spec, prm, seed=1, n=0).size == 0
+    one = lc.random_candidates_gpu(spec, prm, seed=1, n=1)
+    assert one.size == 1 and bool(lc.is_candidate(one, prm, spec)[0])
+    res = lc.walk_arrays(np.zeros(0, dtype=np.uint64), prm, spec)
+    assert res.dst.shape == (0, 1) and res.edges == 0
+    mini, mprm = specs["mini567"], params["mini567"]
+    start = np.array([lc.random_candidate(__import__("random").Random(3), mini, mprm)], dtype=np.uint64)
+    res = lc.walk_arrays(start, mprm, mini, legs=3)
+    hops = lc.candidate_hops(start.tolist(), mprm, mini, legs=3)[0]
+    assert [(int(d), int(w)) for d, w in zip(res.dst[0], res.dist[0])] == hops
+    z = np.zeros(0, dtype=np.uint64)
+    assert all(c.size == 0 for c in lc.sort_edge_arrays(z, z, z))
+    s1 = lc.sort_edge_arrays(np.array([7], dtype=np.uint64), np.array([7], dtype=np.uint64),
+                             np.array([1], dtype=np.uint64))
+    assert [int(c[0]) for c in s1] == [7, 7, 1]
+    assert _batch.first_missing(np.zeros(0, dtype=np.uint64), np.array([5], dtype=np.uint64)) == 0
+    assert _batch.first_missing(np.array([5], dtype=np.uint64), np.zeros(0, dtype=np.uint64)) == 0
