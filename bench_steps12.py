@@ -5,7 +5,7 @@ step-2 prune of the resulting candidates (K3), and a walk of the survivors (K1).
     python bench_steps12.py [--rows-log2 13] [--prune-log2 20] [--depth 3000] [--full]
 
 Prints one JSON line.  --full runs steps 1-3 over the whole slice: every candidate is
-pruned (chunks of 2^26) and every survivor is walked to its next special node.  Parity: the first 4 R2 rows of the slice and a 2048-candidate
+pruned (chunks of 2^28) and every survivor is walked to its next special node.  Parity: the first 4 R2 rows of the slice and a 2048-candidate
 sample of the prune are compared with the C oracle on the host.
 """
 
@@ -153,11 +153,11 @@ def main():
 
 
 def full_slice(args, ctx, sspec, params, cands, stream, torch, N, lc):
-    """Steps 1-3 over the whole slice: prune every candidate (chunks of 2^26 on the
+    """Steps 1-3 over the whole slice: prune every candidate (chunks of 2^28 on the
     device), compact the survivors, walk them all (one lc_walk_device call)."""
     dev = cands.device
     n = cands.numel()
-    chunk = 1 << 26
+    chunk = 1 << 28
     removed = torch.empty(chunk, dtype=torch.uint8, device=dev)
     work = torch.empty(chunk, dtype=torch.int64, device=dev)
     keep = []

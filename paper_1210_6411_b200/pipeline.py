@@ -34,7 +34,7 @@ __all__ = [
     "random_candidates_gpu",
 ]
 
-_PRUNE_CHUNK_GPU = 1 << 22
+_PRUNE_CHUNK_GPU = 1 << 25  # candidates per kernel launch: large, so the tail of the longest traversals amortises
 _ENUM_ROWS_PER_CALL = 1 << 12
 
 
