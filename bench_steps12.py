@@ -5,8 +5,9 @@ step-2 prune of the resulting candidates (K3), and a walk of the survivors (K1).
     python bench_steps12.py [--rows-log2 13] [--prune-log2 20] [--depth 3000] [--full]
 
 Prints one JSON line.  --full runs steps 1-3 over the whole slice: every candidate is
-pruned (chunks of 2^28) and every survivor is walked to its next special node.  Parity: the first 4 R2 rows of the slice and a 2048-candidate
-sample of the prune are compared with the C oracle on the host.
+pruned (chunks of 2^28) and every survivor is walked to its next special node.  Parity:
+the first 4 R2 rows of the slice and a 65536-candidate sample of the prune are compared
+with the C oracle on the host.
 """
 
 from __future__ import annotations
@@ -112,7 +113,7 @@ def main():
     expanded = int(work.sum().item())
     nremoved = int(removed.sum().item())
     # parity on a sample (oracle on host cores)
-    idx = np.linspace(0, npr - 1, min(2048, npr)).astype(np.int64)
+    idx = np.linspace(0, npr - 1, min(1 << 16, npr)).astype(np.int64)
     sample = cands.cpu().numpy().view(np.uint64)[idx]
     t0 = time.perf_counter()
     o_removed, o_work = port.prune(spec, 0x2AAA00, "dfs", args.depth, sample)
