@@ -384,6 +384,33 @@ __device__ __forceinline__ uint32_t pattern_set(uint32_t idx) {
   return static_cast<uint32_t>(w >> ((idx & 15u) << 2)) & 15u;
 }
 
+// The same table under a cheaper index: the three (clock bit, bit above) pairs taken as
+// they sit in the state, pair k at bits 2k..2k+1 with the clock bit low, so the index is
+// three 2-bit field extracts instead of six bit moves.
+constexpr int std_index_ce(int pidx) {
+  const int c1 = pidx & 1, n1 = (pidx >> 1) & 1, c2 = (pidx >> 2) & 1, n2 = (pidx >> 3) & 1;
+  const int c3 = (pidx >> 4) & 1, n3 = (pidx >> 5) & 1;
+  return (c1 << 5) | (n1 << 4) | (c2 << 3) | (n2 << 2) | (c3 << 1) | n3;
+}
+constexpr uint64_t pnibble_word_ce(int w) {
+  uint64_t v = 0;
+  for (int k = 0; k < 16; ++k)
+    for (int q = 0; q < 4; ++q)
+      if ((pattern_mask(q) >> std_index_ce(16 * w + k)) & 1ull) v |= 1ull << (4 * k + q);
+  return v;
+}
+constexpr uint64_t kPNib0 = pnibble_word_ce(0), kPNib1 = pnibble_word_ce(1), kPNib2 = pnibble_word_ce(2),
+                   kPNib3 = pnibble_word_ce(3);
+
+template <class S>
+__device__ __forceinline__ uint32_t pattern_set_of(uint64_t x) {
+  const uint32_t pidx = static_cast<uint32_t>((x >> S::CT1) & 3u) |
+                        (static_cast<uint32_t>((x >> (S::O2 + S::CT2)) & 3u) << 2) |
+                        (static_cast<uint32_t>((x >> (S::O3 + S::CT3)) & 3u) << 4);
+  const uint64_t w = pidx < 32 ? (pidx < 16 ? kPNib0 : kPNib1) : (pidx < 48 ? kPNib2 : kPNib3);
+  return static_cast<uint32_t>(w >> ((pidx & 15u) << 2)) & 15u;
+}
+
 // Child q of the node y: y's predecessor under clock pattern CLOCK_PATTERNS[q], the
 // registers of the pattern unstepped (cipher.py:342-369).
 template <class S>
@@ -461,7 +488,7 @@ struct Ring {
 // the children's table lookups.
 template <class S>
 __device__ __forceinline__ uint32_t child_mask(uint64_t x, uint32_t F) {
-  uint32_t m = pattern_set(table_index<S>(x));
+  uint32_t m = pattern_set_of<S>(x);
   const uint32_t r3 = static_cast<uint32_t>((x >> S::O3) & S::M3);
   if (unstep<S::L3, S::T3>(r3) == F) {
 #pragma unroll
