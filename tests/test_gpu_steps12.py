@@ -261,3 +261,29 @@ def test_enumerate_overflow_returns_prefix(gpu, lc, specs, params):
                                 0x1236, N.u64p(out), cap, C.byref(count))
         assert rc == N.LC_ERR_OVERFLOW and count.value == full.size
         assert (out == full[:cap]).all(), cap
+
+
+def test_prune_random_configs_match_restatement(gpu, lc, specs, params):
+    """Seeded random (cipher, mode, limit, candidate subset) configurations: removed flags
+    and per-candidate `expanded` counters equal the C restatement's (pinned to the
+    reference by prune.json) -- including limits around the ring's depth field and
+    node limits that cut traversals mid-way."""
+    import random
+
+    from oracle import port
+    from paper_1210_6411_b200 import _batch
+
+    rng = random.Random(20261018)
+    pools = {name: lc.random_candidates_gpu(specs[name], params[name], seed=9, n=4096)
+             for name in ("a51", "mini567", "mini789")}
+    for _ in range(12):
+        name = rng.choice(["a51", "a51", "mini567", "mini789"])
+        mode = rng.choice(["dfs", "bfs"])
+        limit = rng.choice([1, 2, 7, 50, 300, 3000, 4095, 4096, 4097, 20000]) if mode == "dfs" else \
+            rng.choice([1, 2, 10, 500, 5000, 100000])
+        pool = pools[name]
+        cands = pool[np.array(sorted(rng.sample(range(pool.size), 1024)))]
+        removed, work = _batch.prune(cands, specs[name], params[name], mode, limit)
+        o_removed, o_work = port.prune(specs[name], params[name].fixed_r3, mode, limit, cands)
+        assert (removed == np.asarray(o_removed).astype(bool)).all(), (name, mode, limit)
+        assert (work == np.asarray(o_work)).all(), (name, mode, limit)
