@@ -117,3 +117,45 @@ def test_sharded_two_ranks_on_one_gpu(gpu):
         assert rows == np.stack(want[:5], 1).tolist(), name
         for r in range(world):
             assert out[(name, r)][1] == [tuple(int(v) for v in p) for p in want[5]], name
+
+
+def _shaped(kind, n, seed):
+    """Edge lists with extreme shapes: a long chain into a 3-cycle, a star into a
+    self-loop, pure cycles, and a binary tree hanging off a 2-cycle."""
+    rng = np.random.default_rng(seed)
+    src = np.unique(rng.integers(1, 1 << 62, size=n, dtype=np.int64)).astype(np.uint64)
+    rng.shuffle(src)
+    m = src.size
+    if kind == "chain":
+        nxt = np.arange(1, m + 1) % m
+        nxt[m - 1] = m - 3
+    elif kind == "star":
+        nxt = np.zeros(m, dtype=np.int64)
+    elif kind == "cycles":
+        nxt = np.arange(1, m + 1) % m
+        nxt[m // 2 - 1] = 0
+        nxt[m - 1] = m // 2
+    else:  # tree
+        nxt = (np.arange(m) - 1) // 2
+        nxt[0] = 1
+        nxt[1] = 0
+    dst = src[nxt]
+    dist = rng.integers(1, 100, size=m).astype(np.uint64)
+    z = np.zeros(m, dtype=np.uint64)
+    order = np.argsort(src)
+    return src[order], dst[order], dist[order], z, z
+
+
+@pytest.mark.parametrize("kind", ["chain", "star", "cycles", "tree"])
+def test_cut_leaves_extreme_shapes(gpu, kind):
+    from oracle import reduce_np
+    from paper_1210_6411_b200.reduce import cut_leaves_tensors
+    from paper_1210_6411_b200.sharded_reduce import cut_leaves_sharded
+
+    cols = _shaped(kind, 20000, 3)
+    want = reduce_np.cut_leaves(*cols)
+    for fn in (cut_leaves_tensors, cut_leaves_sharded):
+        t = _tensors(cols)
+        n_out, passes = fn(*t)
+        assert passes == [tuple(int(v) for v in p) for p in want[5]], (kind, fn.__name__)
+        assert _rows(t, n_out) == np.stack(want[:5], 1).tolist(), (kind, fn.__name__)
