@@ -17,7 +17,8 @@ import numpy as np
 
 from . import _batch
 from ._batch import StrideError, UnsupportedSpecError, WalkResult, default_max_clocks  # noqa: F401
-from .cipher import CandidateParams, CipherSpec, PredecessorTable, unrank_state
+from .cipher import (CandidateParams, CipherSpec, PredecessorTable, clock_forward,  # noqa: F401  (re-exported
+                     minimum_cycle_length, predecessors, shared_table, unrank_state)  # as the reference's module does)
 
 __all__ = [
     "SlicedBatch", "transpose", "untranspose", "clock_sliced", "forward_to_candidate",

@@ -24,7 +24,8 @@ import numpy as np
 from . import _batch
 from . import _native as N
 from .bitslice import forward_to_candidate
-from .cipher import CandidateParams, CipherSpec, PredecessorTable, is_candidate, shared_table
+from .cipher import (CandidateParams, CipherSpec, PredecessorTable, is_candidate,  # noqa: F401  (names the
+                     predecessors, shared_table, unrank_state)  # reference's module also exposes)
 from .records import EdgeRecord
 
 __all__ = [

@@ -3,10 +3,10 @@
 its fixpoint and cycle counting -- plus the edge-output sort that precedes it
 (SURVEY.md §8(f) ranks 1-2).
 
-The whole edge list is held in HBM (SoA columns, csrc/reduce.cu), so a pass is a few
-streaming kernels instead of external sorts over files; the fixpoint records, cycle
-list and per-pass ``leaves_removed`` / ``inner_nodes`` / ``out_size_sum`` equal the
-reference's.  Differences, by design:
+The whole edge list is held in HBM (SoA columns, csrc/reduce.cu) and leaf cutting runs
+as a frontier computation (each pass touches only its own leaves) instead of external
+sorts over files; the fixpoint records, cycle list and per-pass ``leaves_removed`` /
+``inner_nodes`` / ``out_size_sum`` equal the reference's.  Differences, by design:
 
 * ``cut_leaves_to_fixpoint`` checks the conservation invariant the reference intends
   (sum of subtree sizes + surviving records == input records + input sizes).  The
@@ -29,7 +29,8 @@ from typing import Iterable, NamedTuple
 import numpy as np
 
 from . import _native as N
-from .records import EDGE_SIZE, EdgeRecord, read_edge_arrays, write_edge_arrays
+from .records import (EDGE_SIZE, ByteCounter, EdgeRecord, read_edge_arrays, read_edges,  # noqa: F401
+                      write_edge_arrays, write_edges)  # (the last names re-exported as the reference's module does)
 
 __all__ = ["ReduceConfig", "PassStats", "IterationLog", "CycleRecord", "cut_leaves_pass",
            "cut_leaves_to_fixpoint", "count_cycles", "NotAPermutationError", "sort_edge_arrays",
@@ -126,17 +127,21 @@ def sort_edge_arrays(src, dst, dist, subtree_size=None, subtree_depth=None):
 def cut_leaves_arrays(src, dst, dist, subtree_size, subtree_depth, *, max_passes: int = 0):
     """Leaf cutting on arrays (sorted by unique source).  max_passes = 1: one pass;
     0: to the fixpoint.  Returns (src, dst, dist, size, depth, [(leaves, inner, out_size_sum)])."""
-    cols = _cols(src, dst, dist, subtree_size, subtree_depth)
-    n = cols[0].size
     cap = 1 << 16  # per-pass statistics kept (the paper's A5/1 skeleton needs 88 passes)
-    stats = np.zeros((cap, 3), dtype=np.uint64)
-    npass = C.c_uint32(0)
-    nout = C.c_uint64(0)
     ctx = N.context()
-    rc = N.lib.lc_cut_leaves(ctx.handle, n, *(N.u64p(c) for c in cols), int(max_passes), N.u64p(stats), cap,
-                             C.byref(npass), C.byref(nout))
-    if rc != N.LC_OK:
-        _raise(rc)
+    while True:  # a taller forest than `cap` passes: run again with room for every pass
+        cols = _cols(src, dst, dist, subtree_size, subtree_depth)
+        n = cols[0].size
+        stats = np.zeros((cap, 3), dtype=np.uint64)
+        npass = C.c_uint32(0)
+        nout = C.c_uint64(0)
+        rc = N.lib.lc_cut_leaves(ctx.handle, n, *(N.u64p(c) for c in cols), int(max_passes), N.u64p(stats), cap,
+                                 C.byref(npass), C.byref(nout))
+        if rc != N.LC_OK:
+            _raise(rc)
+        if int(npass.value) <= cap:
+            break
+        cap = int(npass.value)
     m = int(nout.value)
     passes = [tuple(int(v) for v in stats[i]) for i in range(min(int(npass.value), cap))]
     return tuple(c[:m] for c in cols) + (passes,)
@@ -155,7 +160,7 @@ def cut_leaves_tensors(src, dst, dist, subtree_size, subtree_depth, *, max_passe
             raise ValueError("columns must be contiguous 64-bit tensors on one CUDA device")
         if c.numel() != src.numel():
             raise ValueError("columns differ in length")
-    cap = 1 << 16
+    cap = max(1, min(src.numel() + 2, 1 << 22))  # a forest of n records has at most n + 1 passes
     stats = np.zeros((cap, 3), dtype=np.uint64)
     npass = C.c_uint32(0)
     nout = C.c_uint64(0)
