@@ -159,3 +159,17 @@ def test_cut_leaves_extreme_shapes(gpu, kind):
         n_out, passes = fn(*t)
         assert passes == [tuple(int(v) for v in p) for p in want[5]], (kind, fn.__name__)
         assert _rows(t, n_out) == np.stack(want[:5], 1).tolist(), (kind, fn.__name__)
+
+
+def test_cut_leaves_arrays_tall_chain_keeps_every_pass(gpu, lc):
+    """A 70,000-record chain into a 3-cycle needs 69,998 passes -- more than the first
+    statistics buffer -- and every pass is reported (closed forms: pass i removes one
+    leaf, leaves m - i inner records, and the survivors' size sum is i)."""
+    cols = _shaped("chain", 70000, 8)
+    m = cols[0].size
+    out = lc.cut_leaves_arrays(*cols)
+    passes = out[5]
+    assert len(passes) == m - 3 + 1
+    assert passes[:-1] == [(1, m - i, i) for i in range(1, m - 2)]
+    assert passes[-1] == (0, 3, m - 3)
+    assert out[0].size == 3 and int(out[3].sum()) == m - 3
