@@ -249,23 +249,24 @@ __device__ __forceinline__ uint32_t slot_r1(uint64_t v, uint32_t a, uint32_t na)
   return (high << (CT1 + 2)) | (static_cast<uint32_t>(__ffs(p) - 1) << CT1) | low;
 }
 
-// Blocks take equal work units (2^16 virtual slots of one R2 row).  A unit's output range is written as 16-byte
-// aligned pairs of states (plus a single head / tail slot), eight pairs per lane per
-// iteration so each thread keeps eight stores in flight: a warp covers 512 consecutive
-// slots per iteration, which span at most three R1 runs when a run has >= 256 values
-// (A5/1), so the runs' (high part, pattern) cost one warp-uniform division per 512
-// slots and a select per slot.  Minis (short runs) use the per-slot form.
+// Blocks take equal work units (2^16 virtual slots of one R2 row).  A unit's output range
+// is written as 32-byte aligned quads of states with 256-bit stores (plus up to three
+// single head / tail slots), four quads per lane per iteration so each thread keeps four
+// stores in flight: a warp covers 512 consecutive slots per iteration, which span at most
+// three R1 runs when a run has >= 256 values (A5/1), so the runs' (high part, pattern)
+// cost one warp-uniform division per 512 slots and a select per slot.  Minis (short runs)
+// use the per-slot form.
 template <class S>
 __global__ void __launch_bounds__(256) enumerate_plane_kernel(uint64_t r2_lo, uint64_t r2_hi, uint32_t F,
                                                               uint64_t* __restrict__ out, uint64_t cap,
                                                               uint64_t* __restrict__ d_count) {
   constexpr int CT1 = S::CT1;
   constexpr uint32_t kLowMask = (1u << CT1) - 1u;
-#ifndef LC_K2_PAIRS
-#define LC_K2_PAIRS 8
+#ifndef LC_K2_QUADS
+#define LC_K2_QUADS 4
 #endif
-  constexpr int kU = LC_K2_PAIRS;  // pairs per lane per iteration (a warp covers 64 * kU slots)
-  constexpr int kSpan = (64 * kU + 255) / 256 + 1;  // runs a chunk can touch (A5/1 runs: 256)
+  constexpr int kU = LC_K2_QUADS;  // 32-byte quads per lane per iteration (a warp covers 128 * kU slots)
+  constexpr int kSpan = (128 * kU + 255) / 256 + 1;  // runs a chunk can touch (A5/1 runs: 256)
   // work units: a row's virtual slots in equal pieces, so blocks get equal work whatever
   // the row's pattern count (1..4 runs per 2^(ct1+2) R1 values)
   constexpr uint64_t kRowSlots = 1ull << S::L1;  // >= any row's virtual slot count
@@ -290,14 +291,19 @@ __global__ void __launch_bounds__(256) enumerate_plane_kernel(uint64_t r2_lo, ui
     const uint64_t row_bits = (r2 << S::O2) | packed_f;
     const uint64_t g0 = base - skip;  // output slot of virtual slot v is g0 + v
     uint64_t v_first = max(skip, u_lo);
-    if ((g0 + v_first) & 1u) {  // odd start: one single slot
-      if (threadIdx.x == 0 && g0 + v_first < cap) out[g0 + v_first] = row_bits | slot_r1<S>(v_first, a, na);
-      ++v_first;
+    // head: single slots up to a 32-byte boundary (at most 3), one thread each
+    const uint64_t to_align = (4u - ((g0 + v_first) & 3u)) & 3u;
+    const uint32_t head = static_cast<uint32_t>(to_align < v_end - v_first ? to_align : v_end - v_first);
+    if (threadIdx.x < head) {
+      const uint64_t v = v_first + threadIdx.x, slot = g0 + v;
+      if (slot < cap) out[slot] = row_bits | slot_r1<S>(v, a, na);
     }
-    const uint64_t npairs = (v_end - v_first) >> 1;
-    if ((v_end - v_first) & 1u) {  // single tail slot
-      const uint64_t v = v_end - 1, slot = g0 + v;
-      if (threadIdx.x == 0 && slot < cap) out[slot] = row_bits | slot_r1<S>(v, a, na);
+    v_first += head;
+    const uint64_t nquads = (v_end - v_first) >> 2;
+    const uint32_t tail = static_cast<uint32_t>((v_end - v_first) & 3u);
+    if (threadIdx.x < tail) {  // tail: at most 3 single slots
+      const uint64_t v = v_first + 4 * nquads + threadIdx.x, slot = g0 + v;
+      if (slot < cap) out[slot] = row_bits | slot_r1<S>(v, a, na);
     }
     uint32_t prank[4];
     {
@@ -308,10 +314,10 @@ __global__ void __launch_bounds__(256) enumerate_plane_kernel(uint64_t r2_lo, ui
         m &= m - 1u;
       }
     }
-    for (uint64_t it = warp; it * (32 * kU) < npairs; it += nwarps) {
-      const uint64_t vbase = v_first + it * (64 * kU);
+    for (uint64_t it = warp; it * (32 * kU) < nquads; it += nwarps) {
+      const uint64_t vbase = v_first + it * (128 * kU);
       uint32_t pre[kSpan] = {}, run0 = 0;
-      if constexpr (kFast) {  // the chunk spans runs run0 .. run0 + 2
+      if constexpr (kFast) {  // the chunk spans runs run0 .. run0 + kSpan - 1
         run0 = static_cast<uint32_t>(vbase >> CT1);
         uint32_t high = run0 / na, rank = run0 - high * na;
 #pragma unroll
@@ -324,34 +330,37 @@ __global__ void __launch_bounds__(256) enumerate_plane_kernel(uint64_t r2_lo, ui
           }
         }
       }
-      ulonglong2 val[kU];
+      uint64_t val[kU][4];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const uint64_t v = vbase + 64 * u + 2 * lane;
-        uint64_t x0, x1;
-        if constexpr (kFast) {
-          const uint32_t d0 = static_cast<uint32_t>(v >> CT1) - run0, d1 = static_cast<uint32_t>((v + 1) >> CT1) - run0;
-          uint32_t q0 = pre[0], q1 = pre[0];
+        const uint64_t v = vbase + 128 * u + 4 * lane;
 #pragma unroll
-          for (int r = 1; r < kSpan; ++r) {
-            q0 = d0 == static_cast<uint32_t>(r) ? pre[r] : q0;
-            q1 = d1 == static_cast<uint32_t>(r) ? pre[r] : q1;
+        for (int e = 0; e < 4; ++e) {
+          if constexpr (kFast) {
+            const uint32_t dd = static_cast<uint32_t>((v + e) >> CT1) - run0;
+            uint32_t qq = pre[0];
+#pragma unroll
+            for (int r = 1; r < kSpan; ++r) qq = dd == static_cast<uint32_t>(r) ? pre[r] : qq;
+            val[u][e] = row_bits | (qq | (static_cast<uint32_t>(v + e) & kLowMask));
+          } else {
+            val[u][e] = row_bits | slot_r1<S>(v + e, a, na);
           }
-          x0 = row_bits | (q0 | (static_cast<uint32_t>(v) & kLowMask));
-          x1 = row_bits | (q1 | (static_cast<uint32_t>(v + 1) & kLowMask));
-        } else {
-          x0 = row_bits | slot_r1<S>(v, a, na);
-          x1 = row_bits | slot_r1<S>(v + 1, a, na);
         }
-        val[u] = make_ulonglong2(x0, x1);
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const uint64_t k = it * (32 * kU) + 32 * u + lane;  // pair index
-        const uint64_t slot = g0 + vbase + 64 * u + 2 * lane;  // even
-        if (k < npairs) {
-          if (slot + 1 < cap) *reinterpret_cast<ulonglong2*>(out + slot) = val[u];
-          else if (slot < cap) out[slot] = val[u].x;
+        const uint64_t k = it * (32 * kU) + 32 * u + lane;  // quad index
+        const uint64_t slot = g0 + vbase + 128 * u + 4 * lane;  // 32-byte aligned
+        if (k < nquads) {
+          if (slot + 3 < cap) {
+            asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(out + slot), "l"(val[u][0]),
+                         "l"(val[u][1]), "l"(val[u][2]), "l"(val[u][3])
+                         : "memory");
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (slot + e < cap) out[slot + e] = val[u][e];
+          }
         }
       }
     }
