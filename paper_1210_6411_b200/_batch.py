@@ -135,7 +135,7 @@ def predecessors(states, spec):
 
 
 def enumerate_rows(spec, params, r2_lo: int, r2_hi: int) -> np.ndarray:
-    """All special nodes with R2 in [r2_lo, r2_hi), ascending (GPU ordered compaction)."""
+    """All special nodes with R2 in [r2_lo, r2_hi), ascending (GPU closed-form writer, K2)."""
     m1 = spec.reg_masks[0]
     cap = max(1, (r2_hi - r2_lo) * m1 // 2 + 1024)
     ctx = N.context()

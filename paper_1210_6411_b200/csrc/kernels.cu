@@ -1,8 +1,8 @@
 // Batch kernels around the walk: the special-node predicate and predecessor batch
-// (cipher.py:342-428), fixed-count clocking (bitslice.clock_sliced), ordered-compaction
+// (cipher.py:342-428), fixed-count clocking (bitslice.clock_sliced), the closed-form
 // enumeration of step 1 (K2, pipeline.enumerate_candidates), the seeded start-set
-// generator (K0), the step-2 prune (K3, pipeline.prune_shallow_segments) and the
-// closure check of build_skeleton_edges.
+// generator (K0, ordered compaction), the step-2 prune (K3,
+// pipeline.prune_shallow_segments) and the closure check of build_skeleton_edges.
 #include <cuda_runtime.h>
 
 #include "lfsr_common.cuh"
@@ -433,12 +433,13 @@ __device__ __forceinline__ uint64_t child_of(uint64_t y, int q) {
 }
 
 // Pending branch points of a lane's traversal: a ring of the kRing deepest nodes that
-// still have unvisited (lower) children, in shared memory ([slot][thread], conflict-free).
-// Backtracking pops the deepest one and jumps straight to its next child instead of
-// climbing the path one forward clock (and one re-expansion) per level.  If the ring
-// overflowed, the oldest entries are gone; once it runs empty the traversal falls back to
-// the stackless climb, which rediscovers them (and an empty ring without overflow means
-// the traversal is complete -- no climb back to the root).
+// still have unvisited (lower) children, in shared memory ([slot][thread], conflict-free),
+// backed by a per-lane spill ring in global memory for the older ones.  Backtracking
+// pops the deepest entry and jumps straight to its next child instead of climbing the
+// path one forward clock (and one re-expansion) per level.  Only when the spill ring
+// overflows are the oldest entries dropped; once ring and spill run empty the traversal
+// falls back to the stackless climb, which rediscovers them (and empty ring and spill
+// without drops mean the traversal is complete -- no climb back to the root).
 #ifndef LC_PRUNE_RING
 #define LC_PRUNE_RING 32
 #endif

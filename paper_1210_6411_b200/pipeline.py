@@ -1,8 +1,8 @@
 """Steps 1-3 orchestration: drop-in for ``lfsrcycles.pipeline`` (reference
 ``pkg/src/lfsrcycles/pipeline.py``).
 
-* ``enumerate_candidates`` -- step 1 on the GPU (K2 ordered compaction), ascending.
-* ``prune_shallow_segments`` -- step 2 on the GPU (K3 stackless reverse DFS/BFS); the
+* ``enumerate_candidates`` -- step 1 on the GPU (K2 closed-form writer), ascending.
+* ``prune_shallow_segments`` -- step 2 on the GPU (K3 reverse DFS with a pending-branch ring); the
   survivor list, ``removed`` and the order-dependent ``expanded`` counter match the
   reference exactly.
 * ``build_skeleton_edges`` -- step 3: the GPU chain walk plus a GPU closure check.
