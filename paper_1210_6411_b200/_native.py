@@ -108,7 +108,7 @@ EXPORTED = tuple(_SIGNATURES)
 def _load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"CUDA library {LIB_PATH} is not built; run `python -m paper_1210_6411_b200.build` "
+            f"CUDA library {LIB_PATH} is not built; run `python paper_1210_6411_b200/build.py` "
             "(or __graft_entry__.build()).  There is no CPU fallback.")
     lib = C.CDLL(LIB_PATH)
     for name, (args, res) in _SIGNATURES.items():

@@ -263,3 +263,21 @@ def test_missing_library_fails_loudly(tmp_path):
     r = subprocess.run([sys.executable, "-c", code], cwd=os.path.dirname(os.path.dirname(__file__)), env=env,
                        capture_output=True, text=True)
     assert r.returncode != 0 and "ImportError" in r.stderr and "no CPU fallback" in r.stderr.replace("There is no", "no")
+
+
+def test_build_entry_does_not_need_the_library(tmp_path):
+    """__graft_entry__.build() must work on a fresh checkout: loading the build script may
+    not import the package (whose __init__ refuses to load without the library)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import importlib.util, os, sys; sys.path.insert(0, '.'); import __graft_entry__; "
+            "assert 'paper_1210_6411_b200' not in sys.modules; "
+            "spec = importlib.util.spec_from_file_location('b', os.path.join('paper_1210_6411_b200', 'build.py')); "
+            "m = importlib.util.module_from_spec(spec); spec.loader.exec_module(m); "
+            "assert 'paper_1210_6411_b200' not in sys.modules; print('ok')")
+    env = dict(os.environ, LFSR_LIB=str(tmp_path / "missing.so"))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stderr
