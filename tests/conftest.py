@@ -20,6 +20,13 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200)")
     config.addinivalue_line("markers", "slow: long-running")
+    # a fresh checkout: compile the library (and the C oracle) once before collecting,
+    # exactly as __graft_entry__.build() does; nvcc cross-compiles without a GPU
+    if not os.environ.get("LFSR_LIB") and not os.path.exists(
+            os.path.join(ROOT, "paper_1210_6411_b200", "_lib", "liblfsr_b200.so")):
+        import __graft_entry__
+
+        __graft_entry__.build()
 
 
 def golden_npz(name):
