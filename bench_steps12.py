@@ -5,7 +5,7 @@ step-2 prune of the resulting candidates (K3), and a walk of the survivors (K1).
     python bench_steps12.py [--rows-log2 13] [--prune-log2 20] [--depth 3000] [--full]
 
 Prints one JSON line.  --full runs steps 1-3 over the whole slice: every candidate is
-pruned (chunks of 2^28) and every survivor is walked to its next special node.  Parity:
+pruned (one launch; --prune-chunk-log2 splits it) and every survivor is walked to its next special node.  Parity:
 the first 4 R2 rows of the slice and a 65536-candidate sample of the prune are compared
 with the C oracle on the host.
 """
@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--depth", type=int, default=3000)     # the paper's DFS depth
     ap.add_argument("--walk-log2", type=int, default=14)
     ap.add_argument("--full", action="store_true")
+    ap.add_argument("--prune-chunk-log2", type=int, default=31)  # --full: candidates per prune launch
     args = ap.parse_args()
 
     import torch
@@ -154,11 +155,13 @@ def main():
 
 
 def full_slice(args, ctx, sspec, params, cands, stream, torch, N, lc):
-    """Steps 1-3 over the whole slice: prune every candidate (chunks of 2^28 on the
-    device), compact the survivors, walk them all (one lc_walk_device call)."""
+    """Steps 1-3 over the whole slice: prune every candidate (one lc_prune_device launch
+    per 2^prune_chunk_log2 candidates -- by default the whole slice at once, so the
+    heavy-tailed traversals leave one tail, not one per chunk), compact the survivors,
+    walk them all (one lc_walk_device call)."""
     dev = cands.device
     n = cands.numel()
-    chunk = 1 << 28
+    chunk = min(n, 1 << args.prune_chunk_log2)
     removed = torch.empty(chunk, dtype=torch.uint8, device=dev)
     work = torch.empty(chunk, dtype=torch.int64, device=dev)
     keep = []
@@ -202,7 +205,7 @@ def full_slice(args, ctx, sspec, params, cands, stream, torch, N, lc):
             "walks": ns, "transitions": tr, "walk_s": walk_s, "transitions_per_s": tr / walk_s,
             "min_dist": int(stats[N.ST_MIN]), "max_dist": int(stats[N.ST_MAX]),
             "destinations_are_special_nodes": ok,
-            "steps_1_to_3_s": prune_s + walk_s}
+            "prune_launch_candidates": chunk, "steps_1_to_3_s": prune_s + walk_s}
 
 
 if __name__ == "__main__":
