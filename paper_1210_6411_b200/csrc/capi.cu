@@ -633,7 +633,8 @@ int lc_prune_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int32_t
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
   LC_CUDA(ctx->pq.ensure(8));
   LC_CUDA(cudaMemsetAsync(ctx->pq.p, 0, 8, st));
-  const int blocks = lc::prune_blocks_per_sm(id) * ctx->sms;
+  const int ring = lc::prune_ring_for(n);
+  const int blocks = lc::prune_blocks_per_sm(id, ring) * ctx->sms;
 #ifndef LC_PRUNE_SPILL
 #define LC_PRUNE_SPILL 512
 #endif
@@ -643,7 +644,7 @@ int lc_prune_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int32_t
   if (const char* env = getenv("LFSR_PRUNE_SPILL")) spill_cap = static_cast<uint32_t>(strtoul(env, nullptr, 10));
   if (spill_cap) LC_CUDA(ctx->spill.ensure(lc::prune_spill_bytes(blocks, spill_cap)));
   LC_CUDA(lc::launch_prune(id, static_cast<uint32_t>(fixed_r3), mode, limit, d_cands, n, d_removed, d_work,
-                           ctx->pq.as<unsigned long long>(), spill_cap ? ctx->spill.p : nullptr, spill_cap, blocks,
+                           ctx->pq.as<unsigned long long>(), spill_cap ? ctx->spill.p : nullptr, spill_cap, ring, blocks,
                            st));
   g_launches += 1;
   return LC_OK;

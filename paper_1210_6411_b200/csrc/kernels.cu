@@ -5,6 +5,8 @@
 // pipeline.prune_shallow_segments) and the closure check of build_skeleton_edges.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "lfsr_common.cuh"
 #include "lfsr_internal.h"
 
@@ -376,26 +378,10 @@ __global__ void __launch_bounds__(256) enumerate_plane_kernel(uint64_t r2_lo, ui
 // counter matches exactly.  BFS mode (pipeline.py:147-160) only needs the segment size
 // capped at node_limit + 1, which is order-independent.
 
-// The predecessor table as 64 nibbles (bit q of nibble idx = pattern q consistent at
-// table index idx), packed in four 64-bit immediates.
-constexpr uint64_t nibble_word_ce(int w) {
-  uint64_t v = 0;
-  for (int k = 0; k < 16; ++k)
-    for (int q = 0; q < 4; ++q)
-      if ((pattern_mask(q) >> (16 * w + k)) & 1ull) v |= 1ull << (4 * k + q);
-  return v;
-}
-constexpr uint64_t kNib0 = nibble_word_ce(0), kNib1 = nibble_word_ce(1), kNib2 = nibble_word_ce(2),
-                   kNib3 = nibble_word_ce(3);
-
-__device__ __forceinline__ uint32_t pattern_set(uint32_t idx) {
-  const uint64_t w = idx < 32 ? (idx < 16 ? kNib0 : kNib1) : (idx < 48 ? kNib2 : kNib3);
-  return static_cast<uint32_t>(w >> ((idx & 15u) << 2)) & 15u;
-}
-
-// The same table under a cheaper index: the three (clock bit, bit above) pairs taken as
-// they sit in the state, pair k at bits 2k..2k+1 with the clock bit low, so the index is
-// three 2-bit field extracts instead of six bit moves.
+// The predecessor table as 64 nibbles (bit q of a nibble = pattern q consistent), packed
+// in four 64-bit immediates and indexed by the three (clock bit, bit above) pairs taken as
+// they sit in the state -- pair k at bits 2k..2k+1, clock bit low -- so the index is three
+// 2-bit field extracts instead of table_index's six bit moves.
 constexpr int std_index_ce(int pidx) {
   const int c1 = pidx & 1, n1 = (pidx >> 1) & 1, c2 = (pidx >> 2) & 1, n2 = (pidx >> 3) & 1;
   const int c3 = (pidx >> 4) & 1, n3 = (pidx >> 5) & 1;
@@ -432,7 +418,7 @@ __device__ __forceinline__ uint64_t child_of(uint64_t y, int q) {
   return static_cast<uint64_t>(p1) | (static_cast<uint64_t>(p2) << S::O2) | (static_cast<uint64_t>(p3) << S::O3);
 }
 
-// Pending branch points of a lane's traversal: a ring of the kRing deepest nodes that
+// Pending branch points of a lane's traversal: a ring of the R deepest nodes that
 // still have unvisited (lower) children, in shared memory ([slot][thread], conflict-free),
 // backed by a per-lane spill ring in global memory for the older ones.  Backtracking
 // pops the deepest entry and jumps straight to its next child instead of climbing the
@@ -440,14 +426,14 @@ __device__ __forceinline__ uint64_t child_of(uint64_t y, int q) {
 // overflows are the oldest entries dropped; once ring and spill run empty the traversal
 // falls back to the stackless climb, which rediscovers them (and empty ring and spill
 // without drops mean the traversal is complete -- no climb back to the root).
-#ifndef LC_PRUNE_RING
-#define LC_PRUNE_RING 32
-#endif
+// Ring depth is a template parameter: deep rings spill less (the spill round trip sits
+// on a lane's critical path, which bounds the tail of small batches), shallow rings fit
+// more warps per SM (throughput over large batches); launch_prune picks per batch size.
 #ifndef LC_PRUNE_THREADS
 #define LC_PRUNE_THREADS 128
 #endif
-constexpr int kRing = LC_PRUNE_RING;
-constexpr int kPruneThreads = LC_PRUNE_THREADS;  // the ring takes kRing * 10 B per thread of shared memory
+constexpr int kRingDeep = 32, kRingWide = 20;
+constexpr int kPruneThreads = LC_PRUNE_THREADS;  // a ring of R entries takes R * 10 B per thread of shared memory
 constexpr uint64_t kDepthCap = 1u << 12;  // ring entries hold depths below this (12-bit field)
 constexpr int kTailBurst = 32;  // steps per warp vote once no candidate is left to take
 #ifndef LC_PRUNE_BULK_BURST
@@ -455,8 +441,9 @@ constexpr int kTailBurst = 32;  // steps per warp vote once no candidate is left
 #endif
 constexpr int kBulkBurst = LC_PRUNE_BULK_BURST;  // steps per warp vote while candidates remain
 
+template <int R>
 struct Ring {
-  uint64_t* node;  // [kRing][kPruneThreads]: the branch node
+  uint64_t* node;  // [R][kPruneThreads]: the branch node
   uint16_t* dm;    //                         depth << 4 | remaining child mask
   uint64_t* snode; // this lane's spill ring in global memory (older entries), [scap]
   uint16_t* sdm;
@@ -465,8 +452,8 @@ struct Ring {
   __device__ __forceinline__ uint32_t at(uint32_t slot) const { return slot * kPruneThreads + threadIdx.x; }
   __device__ __forceinline__ void push(uint64_t y, uint64_t d, uint32_t mask) {
     if (d >= kDepthCap) return;  // no room for the depth: found again by climbing (see prune_step)
-    const uint32_t next = top + 1 == static_cast<uint32_t>(kRing) ? 0u : top + 1;
-    if (cnt == kRing) {  // full: the oldest entry (about to be overwritten) moves to the spill ring
+    const uint32_t next = top + 1 == static_cast<uint32_t>(R) ? 0u : top + 1;
+    if (cnt == R) {  // full: the oldest entry (about to be overwritten) moves to the spill ring
       if (scap) {
         if (scnt == scap) {  // spill full too: drop its oldest entry (the climb recovers it)
           sbase = sbase + 1 == scap ? 0u : sbase + 1;
@@ -516,8 +503,8 @@ __device__ __forceinline__ uint32_t child_mask(uint64_t x, uint32_t F) {
 // point) only pick the source node and child index, then share one child computation,
 // so a warp's lanes diverge only over a few selects and the ring access.
 // Returns 0 while running, 1 = finished shallow, 2 = finished deep (not shallow).
-template <class S>
-__device__ __forceinline__ int prune_step(uint64_t& x, uint64_t& d, uint64_t& acc, bool& climb, Ring& ring,
+template <class S, int R>
+__device__ __forceinline__ int prune_step(uint64_t& x, uint64_t& d, uint64_t& acc, bool& climb, Ring<R>& ring,
                                           uint32_t F, int mode, uint64_t limit) {
   uint64_t src = x;
   uint32_t q = 0;
@@ -575,7 +562,7 @@ __device__ __forceinline__ int prune_step(uint64_t& x, uint64_t& d, uint64_t& ac
     if (ring.cnt == 0u && ring.scnt) {  // the ring ran dry: bring back the newest spilled entry
       const uint32_t j = ring.sbase + ring.scnt - 1u;
       const uint32_t k = j < ring.scap ? j : j - ring.scap;
-      ring.top = ring.top + 1 == static_cast<uint32_t>(kRing) ? 0u : ring.top + 1;
+      ring.top = ring.top + 1 == static_cast<uint32_t>(R) ? 0u : ring.top + 1;
       ring.node[ring.at(ring.top)] = ring.snode[k];
       ring.dm[ring.at(ring.top)] = ring.sdm[k];
       ring.cnt = 1;
@@ -591,7 +578,7 @@ __device__ __forceinline__ int prune_step(uint64_t& x, uint64_t& d, uint64_t& ac
       if (rest) {
         ring.dm[slot] = static_cast<uint16_t>((dm & ~15u) | rest);
       } else {
-        ring.top = ring.top == 0u ? kRing - 1 : ring.top - 1;
+        ring.top = ring.top == 0u ? R - 1 : ring.top - 1;
         --ring.cnt;
       }
       d = (dm >> 4) + 1;
@@ -610,20 +597,20 @@ __device__ __forceinline__ int prune_step(uint64_t& x, uint64_t& d, uint64_t& ac
 // Persistent: every lane runs its own traversal and takes the next candidate as soon as
 // it finishes (tickets aggregated over the lanes that need one), so a warp is never held
 // up by its deepest segment.
-template <class S>
+template <class S, int R>
 __global__ void __launch_bounds__(kPruneThreads) prune_kernel(const uint64_t* __restrict__ cands, uint64_t n,
                                                          uint32_t F, int mode, uint64_t limit,
                                                          uint8_t* __restrict__ removed,
                                                          uint64_t* __restrict__ work,
                                                          unsigned long long* queue, uint64_t* spill_node,
                                                          uint16_t* spill_dm, uint32_t spill_cap) {
-  __shared__ uint64_t ring_node[kRing * kPruneThreads];
-  __shared__ uint16_t ring_dm[kRing * kPruneThreads];
+  __shared__ uint64_t ring_node[R * kPruneThreads];
+  __shared__ uint16_t ring_dm[R * kPruneThreads];
   const uint32_t lane = threadIdx.x & 31u;
   uint64_t i = 0, x = 0, d = 0, acc = 0;
   bool have = false, climb = false, drained = false;
   const uint64_t gtid = blockIdx.x * static_cast<uint64_t>(kPruneThreads) + threadIdx.x;
-  Ring ring{ring_node, ring_dm, spill_node ? spill_node + gtid * spill_cap : nullptr,
+  Ring<R> ring{ring_node, ring_dm, spill_node ? spill_node + gtid * spill_cap : nullptr,
             spill_dm ? spill_dm + gtid * spill_cap : nullptr, 0, 0, 0, spill_node ? spill_cap : 0u, 0, false};
   for (;;) {
     if (!drained) {
@@ -654,10 +641,10 @@ __global__ void __launch_bounds__(kPruneThreads) prune_kernel(const uint64_t* __
     if (have) {
       // once the candidates are drained nothing can be refilled: run bursts of steps
       // between warp votes (the tail is latency-bound on the longest traversals)
-      int r = prune_step<S>(x, d, acc, climb, ring, F, mode, limit);
+      int r = prune_step<S, R>(x, d, acc, climb, ring, F, mode, limit);
       const int burst = drained ? kTailBurst : kBulkBurst;
 #pragma unroll 1
-      for (int k = 1; k < burst && r == 0; ++k) r = prune_step<S>(x, d, acc, climb, ring, F, mode, limit);
+      for (int k = 1; k < burst && r == 0; ++k) r = prune_step<S, R>(x, d, acc, climb, ring, F, mode, limit);
       if (r != 0) {
         removed[i] = r == 1 ? 1 : 0;
         work[i] = acc;
@@ -743,27 +730,45 @@ uint64_t prune_spill_bytes(int blocks, uint32_t cap) {
   return static_cast<uint64_t>(blocks) * kPruneThreads * cap * (8 + 2) + 512;
 }
 
+int prune_ring_for(uint64_t n) {
+  if (const char* env = getenv("LFSR_PRUNE_RING")) {  // testing / A-B: force a variant
+    const int r = atoi(env);
+    if (r == kRingDeep || r == kRingWide) return r;
+  }
+  return n >= (uint64_t{1} << 24) ? kRingWide : kRingDeep;
+}
+
+template <int R>
+static int blocks_per_sm(SpecId id) {
+  int b = 1;
+  switch (id) {
+    case SpecId::A51: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, prune_kernel<A51, R>, kPruneThreads, 0); break;
+    case SpecId::MINI567: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, prune_kernel<MINI567, R>, kPruneThreads, 0); break;
+    case SpecId::MINI789: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, prune_kernel<MINI789, R>, kPruneThreads, 0); break;
+    default: break;
+  }
+  return b > 0 ? b : 1;
+}
+
+int prune_blocks_per_sm(SpecId id, int ring) {
+  return ring == kRingWide ? blocks_per_sm<kRingWide>(id) : blocks_per_sm<kRingDeep>(id);
+}
+
 cudaError_t launch_prune(SpecId id, uint32_t F, int mode, uint64_t limit, const uint64_t* cands,
                          uint64_t n, uint8_t* removed, uint64_t* work, unsigned long long* queue,
-                         void* spill, uint32_t spill_cap, int blocks, cudaStream_t stream) {
+                         void* spill, uint32_t spill_cap, int ring, int blocks, cudaStream_t stream) {
   uint64_t* spill_node = spill ? static_cast<uint64_t*>(spill) : nullptr;
   uint16_t* spill_dm =
       spill ? reinterpret_cast<uint16_t*>(spill_node + static_cast<uint64_t>(blocks) * kPruneThreads * spill_cap)
             : nullptr;
-  LC_DISPATCH(id, prune_kernel<S><<<blocks, kPruneThreads, 0, stream>>>(cands, n, F, mode, limit, removed, work,
-                                                                   queue, spill_node, spill_dm, spill_cap);
-              return cudaGetLastError());
-}
-
-int prune_blocks_per_sm(SpecId id) {
-  int b = 1;
-  switch (id) {
-    case SpecId::A51: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, prune_kernel<A51>, kPruneThreads, 0); break;
-    case SpecId::MINI567: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, prune_kernel<MINI567>, kPruneThreads, 0); break;
-    case SpecId::MINI789: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, prune_kernel<MINI789>, kPruneThreads, 0); break;
-    default: break;
+  if (ring == kRingWide) {
+    LC_DISPATCH(id, prune_kernel<S, kRingWide><<<blocks, kPruneThreads, 0, stream>>>(
+                        cands, n, F, mode, limit, removed, work, queue, spill_node, spill_dm, spill_cap);
+                return cudaGetLastError());
   }
-  return b > 0 ? b : 1;
+  LC_DISPATCH(id, prune_kernel<S, kRingDeep><<<blocks, kPruneThreads, 0, stream>>>(
+                      cands, n, F, mode, limit, removed, work, queue, spill_node, spill_dm, spill_cap);
+              return cudaGetLastError());
 }
 
 cudaError_t launch_first_missing(const uint64_t* set, uint64_t m, const uint64_t* q, uint64_t n,

@@ -105,8 +105,11 @@ uint64_t random_scratch_words(uint64_t trials);
 uint64_t prune_spill_bytes(int blocks, uint32_t cap);
 cudaError_t launch_prune(SpecId id, uint32_t F, int mode, uint64_t limit, const uint64_t* cands,
                          uint64_t n, uint8_t* removed, uint64_t* work, unsigned long long* queue,
-                         void* spill, uint32_t spill_cap, int blocks, cudaStream_t stream);
-int prune_blocks_per_sm(SpecId id);
+                         void* spill, uint32_t spill_cap, int ring, int blocks, cudaStream_t stream);
+// Ring depth (entries per lane in shared memory) for a batch of n candidates: the deep
+// ring below 2^24 (tail-bound), the wide-occupancy one above (LFSR_PRUNE_RING forces 20/32).
+int prune_ring_for(uint64_t n);
+int prune_blocks_per_sm(SpecId id, int ring);
 
 cudaError_t measure_lop3_peak(int sms, double* ops_per_s, double* sm_mhz);
 

@@ -201,13 +201,15 @@ def test_prune_deep_limit_matches_oracle(gpu, lc, specs, params):
         assert (work == np.asarray(o_work)).all(), limit
 
 
-@pytest.mark.parametrize("spill", ["0", "1", "3"])
-def test_prune_small_spill_matches_reference(gpu, lc, specs, params, spill):
-    """Tiny (or no) global spill behind the 32-entry ring forces the drop-oldest +
+@pytest.mark.parametrize("spill,ring", [("0", "32"), ("1", "32"), ("3", "32"), ("0", "20"), ("3", "20"),
+                                       ("512", "20")])
+def test_prune_small_spill_matches_reference(gpu, lc, specs, params, spill, ring):
+    """Tiny (or no) global spill behind the shared-memory ring (32 entries, or the
+    20-entry variant launched for batches of 2^24 and more) forces the drop-oldest +
     stackless-climb fallback on deep traversals; survivors and the per-candidate LIFO
     `expanded` counters must still equal the reference's (prune.json) and the C
-    restatement.  The kernel reads LFSR_PRUNE_SPILL at launch, so it runs in a child
-    process."""
+    restatement.  The kernel reads LFSR_PRUNE_SPILL / LFSR_PRUNE_RING at launch, so it
+    runs in a child process."""
     import json
     import os
     import subprocess
@@ -239,7 +241,7 @@ ok = ok and (removed == np.asarray(o_removed).astype(bool)).all() and (work == n
 print(json.dumps({"ok": bool(ok)}))
 '''
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, LFSR_PRUNE_SPILL=spill)
+    env = dict(os.environ, LFSR_PRUNE_SPILL=spill, LFSR_PRUNE_RING=ring)
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert json.loads(r.stdout.strip().splitlines()[-1])["ok"]
@@ -263,13 +265,16 @@ def test_enumerate_overflow_returns_prefix(gpu, lc, specs, params):
         assert (out == full[:cap]).all(), cap
 
 
-def test_prune_random_configs_match_restatement(gpu, lc, specs, params):
+@pytest.mark.parametrize("ring", ["32", "20"])
+def test_prune_random_configs_match_restatement(gpu, lc, specs, params, ring, monkeypatch):
     """Seeded random (cipher, mode, limit, candidate subset) configurations: removed flags
     and per-candidate `expanded` counters equal the C restatement's (pinned to the
     reference by prune.json) -- including limits around the ring's depth field and
-    node limits that cut traversals mid-way."""
+    node limits that cut traversals mid-way -- for both ring variants (the launch reads
+    LFSR_PRUNE_RING)."""
     import random
 
+    monkeypatch.setenv("LFSR_PRUNE_RING", ring)
     from oracle import port
     from paper_1210_6411_b200 import _batch
 
