@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--walk-log2", type=int, default=14)
     ap.add_argument("--full", action="store_true")
     ap.add_argument("--prune-chunk-log2", type=int, default=31)  # --full: candidates per prune launch
+    ap.add_argument("--skip-walk", action="store_true")  # --full: prune only (A/B of K3 variants)
     args = ap.parse_args()
 
     import torch
@@ -181,6 +182,9 @@ def full_slice(args, ctx, sspec, params, cands, stream, torch, N, lc):
     prune_s = e0.elapsed_time(e1) / 1e3
     surv = torch.cat(keep)
     ns = surv.numel()
+    if args.skip_walk:
+        return {"candidates": n, "prune_depth": args.depth, "survivors": ns, "expanded": expanded,
+                "prune_s": prune_s, "expansions_per_s": expanded / prune_s, "prune_launch_candidates": chunk}
     dst = torch.empty(ns, dtype=torch.int64, device=dev)
     dist = torch.empty(ns, dtype=torch.int64, device=dev)
     words = N.ST_HEADER + 2

@@ -432,7 +432,10 @@ __device__ __forceinline__ uint64_t child_of(uint64_t y, int q) {
 #ifndef LC_PRUNE_THREADS
 #define LC_PRUNE_THREADS 128
 #endif
-constexpr int kRingDeep = 32, kRingWide = 20;
+#ifndef LC_PRUNE_RING_WIDE
+#define LC_PRUNE_RING_WIDE 20
+#endif
+constexpr int kRingDeep = 32, kRingWide = LC_PRUNE_RING_WIDE;
 constexpr int kPruneThreads = LC_PRUNE_THREADS;  // a ring of R entries takes R * 10 B per thread of shared memory
 constexpr uint64_t kDepthCap = 1u << 12;  // ring entries hold depths below this (12-bit field)
 constexpr int kTailBurst = 32;  // steps per warp vote once no candidate is left to take
