@@ -1,4 +1,4 @@
-"""Config 2 parity at scale (opt-in, LFSR_SLOW=1): the first 2^18 starts of the bench's K0
+"""Config 2 parity at scale (opt-in, LFSR_SLOW=1): the first 2^18 (LFSR_C2_LOG2 sets it) starts of the bench's K0
 workload (2^24 special A5/1 nodes, seed 12106411) walked on the GPU and by the C
 restatement of the reference (oracle/lfsr_oracle.c, pinned to the reference's own
 config-1 run) on all host cores -- about 4 minutes of CPU.  Bit-exact edges required.
