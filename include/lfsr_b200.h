@@ -107,6 +107,11 @@ int lc_walk(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3, const uint64_t 
             uint64_t n, uint64_t stride, uint64_t max_clocks, uint32_t legs, uint32_t refill,
             uint64_t *dest, uint64_t *dist, uint64_t hist_lo, uint32_t hist_shift,
             uint32_t hist_bins, uint64_t *stats);
+/* lc_walk on device buffers, enqueued on `stream` and returning without a sync.  Lane-mode
+ * walks with more starts than one wave of the GPU's warp schedulers holds queue up to
+ * four launches: warps drained below half occupancy park their lanes and the next launch
+ * resumes them packed (item count read on the device).  Results are identical to one
+ * launch; the environment variable LFSR_WALK_NO_PARK forces one launch (A/B testing). */
 int lc_walk_device(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3,
                    const uint64_t *d_starts, uint64_t n, uint64_t stride, uint64_t max_clocks,
                    uint32_t legs, uint32_t refill, uint64_t *d_dest, uint64_t *d_dist,

@@ -264,7 +264,8 @@ struct WalkArgs {
 // reset).  pool != null: drained warps park below park_below live lanes.
 int walk_launch(lc_ctx* ctx, const WalkArgs& a, const uint64_t* d_starts, const lc::ResumeRec* resume, uint64_t n,
                 uint64_t* d_dest, uint64_t* d_dist, uint64_t* d_stats, lc::ResumeRec* pool,
-                unsigned long long* pool_count, uint32_t park_below, cudaStream_t st) {
+                unsigned long long* pool_count, uint32_t park_below, cudaStream_t st,
+                const unsigned long long* n_dev = nullptr, uint64_t park_min = 0) {
   int rc = ensure_smsp_map(ctx);
   if (rc) return rc;
   if ((rc = ensure_need3(ctx, a.id, a.fixed_r3))) return rc;
@@ -272,14 +273,16 @@ int walk_launch(lc_ctx* ctx, const WalkArgs& a, const uint64_t* d_starts, const 
   const int per_sm = lc::walk_blocks_per_sm(a.id, static_f);
   const uint64_t lanes_per_block = lc::kWalkThreads * 32ull;
   const uint64_t max_blocks = static_cast<uint64_t>(per_sm) * ctx->sms;
-  const uint64_t want = (n + lanes_per_block - 1) / lanes_per_block;
+  // n_dev: n is only an upper bound (the count is on the device), so cover the whole GPU
+  const uint64_t want = n_dev ? max_blocks : (n + lanes_per_block - 1) / lanes_per_block;
   const int blocks = static_cast<int>(std::max<uint64_t>(1, std::min(max_blocks, want)));
   // auto (refill == 0): single-hop walks whose starts are all special-node-like run with
   // whole-warp refill (decided on the device by the mode probe); everything else per lane
   const bool auto_mode = resume == nullptr && a.refill == 0 && a.legs == 1;
   const uint32_t refill_min = (resume || a.refill == 0) ? 1u : a.refill;
   // one queue per warp scheduler when the persistent grid covers every SM
-  const uint32_t nq = (ctx->mapped_sms == ctx->sms && static_cast<uint64_t>(blocks) == max_blocks)
+  // (not for a resume round sized on the device: most of its blocks exit at once)
+  const uint32_t nq = (ctx->mapped_sms == ctx->sms && static_cast<uint64_t>(blocks) == max_blocks && !n_dev)
                           ? 4u * static_cast<uint32_t>(ctx->sms) : 1u;
 
   LC_CUDA(ctx->meta.ensure(static_cast<size_t>(blocks) * lanes_per_block * sizeof(lc::LaneMeta)));
@@ -324,6 +327,8 @@ int walk_launch(lc_ctx* ctx, const WalkArgs& a, const uint64_t* d_starts, const 
   p.pool = pool;
   p.pool_count = pool_count;
   p.park_below = pool ? park_below : 0u;
+  p.n_dev = n_dev;
+  p.park_min = park_min;
   p.need3 = ctx->need3.as<uint32_t>();
   p.run_if_mode = ~0u;
   // Re-arming pays for lanes that would otherwise be checked for long stretches: lane
@@ -381,7 +386,29 @@ int lc_walk_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const ui
   a.hist_bins = hist_bins;
   LC_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
-  return walk_launch(ctx, a, d_starts, nullptr, n, d_dest, d_dist, d_stats, nullptr, nullptr, 0, st);
+  // Lane parking without a host sync (the call stays asynchronous): a fixed number of
+  // resume rounds is queued, each reading its item count (the previous round's parked
+  // lanes) on the device; a round with nothing parked exits at once, and the last round
+  // never parks, so every walk completes.  Whole-warp launches never park (kernel-side).
+  const uint64_t park_threshold = 4ull * static_cast<uint64_t>(ctx->sms) * 1024ull;
+  if (n <= park_threshold || getenv("LFSR_WALK_NO_PARK") != nullptr)
+    return walk_launch(ctx, a, d_starts, nullptr, n, d_dest, d_dist, d_stats, nullptr, nullptr, 0, st);
+  constexpr int kRounds = 4;
+  const uint64_t cap = std::min<uint64_t>(n, 8ull * park_threshold);
+  LC_CUDA(ctx->pool_a.ensure(cap * sizeof(lc::ResumeRec)));
+  LC_CUDA(ctx->pool_b.ensure(cap * sizeof(lc::ResumeRec)));
+  LC_CUDA(ctx->pq.ensure(16 + kRounds * sizeof(unsigned long long)));
+  lc::ResumeRec* pools[2] = {ctx->pool_a.as<lc::ResumeRec>(), ctx->pool_b.as<lc::ResumeRec>()};
+  unsigned long long* counts = ctx->pq.as<unsigned long long>() + 2;  // [1] is lc_walk's
+  LC_CUDA(cudaMemsetAsync(counts, 0, kRounds * sizeof(unsigned long long), st));
+  for (int round = 0; round < kRounds; ++round) {
+    const bool last = round == kRounds - 1;
+    const int rc2 = walk_launch(ctx, a, d_starts, round ? pools[(round - 1) & 1] : nullptr, round ? cap : n, d_dest,
+                                d_dist, d_stats, last ? nullptr : pools[round & 1], counts + round, 512u, st,
+                                round ? counts + round - 1 : nullptr, park_threshold);
+    if (rc2) return rc2;
+  }
+  return LC_OK;
 }
 
 // Host-buffer walk.  Runs in rounds: warps that drain below half occupancy park their

@@ -65,6 +65,8 @@ struct WalkParams {
   const uint32_t* need3;       // [2^l3] R3 clocks from each R3 value to fixed_r3 (null: none)
   uint32_t run_if_mode;        // ~0: always run; else run only if *mode_word equals it
   uint32_t pad3;
+  const unsigned long long* n_dev;  // resume round queued without a host sync: item count on the device (else null)
+  uint64_t park_min;                // park only while the round has more than this many items
 };
 
 // Launchers (defined in the .cu files); all enqueue on `stream`.

@@ -162,6 +162,8 @@ struct WalkShared {
   uint32_t open[kWalkThreads / 32];         // queues not yet exhausted for this warp
   uint32_t warp_mode;                       // 1: whole-warp refill (1024-start items)
   uint32_t refill_min;                      // lane mode: refill at this many idle lanes
+  uint32_t park;                            // this launch parks drained warps (lane mode only)
+  unsigned long long n;                     // items in this launch (p.n, or *p.n_dev)
 };
 
 constexpr uint32_t kWarpItem = 1024;  // starts per queue item in whole-warp mode
@@ -249,7 +251,7 @@ __device__ __forceinline__ void lane_refill(const WalkParams& p, volatile WalkSh
   const uint32_t tid = tid_x(), lane = tid & 31u, w = tid >> 5;
   const uint64_t gtid = static_cast<uint64_t>(ctaid_x()) * kWalkThreads + tid;
   LaneMeta* const meta = p.meta + gtid * 32u;
-  const uint64_t items = p.n;  // chunk == 1: item == start index
+  const uint64_t items = sh.n;  // chunk == 1: item == start index
   const uint64_t t = sh.t[w];
   for (;;) {
     const uint32_t idle = ~sh.active[tid];
@@ -472,6 +474,9 @@ template <class S, bool SF, bool RA>
 __global__ void __launch_bounds__(kWalkThreads, LC_WALK_MIN_BLOCKS) walk_kernel(const WalkParams p) {
   // auto mode launches both variants; the one not meant for the probed mode exits
   if (p.run_if_mode != ~0u && *p.mode_word != p.run_if_mode) return;
+  // resume round sized on the device: only the blocks its parked lanes fill run, so the
+  // lanes stay packed into few warps (the grid covers the bound, not the count)
+  if (p.n_dev && static_cast<uint64_t>(ctaid_x()) * (kWalkThreads * 32ull) >= *p.n_dev) return;
   __shared__ WalkShared sh_storage;
   volatile WalkShared& sh = sh_storage;
   {
@@ -495,6 +500,10 @@ __global__ void __launch_bounds__(kWalkThreads, LC_WALK_MIN_BLOCKS) walk_kernel(
       const uint32_t warp_mode = p.mode_word ? *p.mode_word : (p.chunk > 1u ? 1u : 0u);
       sh.warp_mode = warp_mode;
       sh.refill_min = warp_mode ? kWarpItem : p.refill_min;
+      const uint64_t n = p.n_dev ? *p.n_dev : p.n;
+      sh.n = n;
+      // whole-warp walks end together (near-constant lengths): nothing to pack
+      sh.park = p.pool != nullptr && !warp_mode && n > p.park_min;
     }
     __syncthreads();
   }
@@ -522,7 +531,7 @@ __global__ void __launch_bounds__(kWalkThreads, LC_WALK_MIN_BLOCKS) walk_kernel(
         if (!sh.open[w]) break;
         continue;
       }
-      if (p.pool && !sh.open[w] &&
+      if (sh.park && !sh.open[w] &&
           __reduce_add_sync(kFull, static_cast<uint32_t>(__popc(sh.active[tid]))) < p.park_below) {
         park_lanes<S>(p, sh, s);
         break;
