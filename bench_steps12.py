@@ -27,33 +27,33 @@ sys.path.insert(0, ROOT)
 R2_0 = 0x2AAA  # first R2 row of the slice
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--rows-log2", type=int, default=13)   # 2^13 rows x (2^19-1) = 2^32 states
-    ap.add_argument("--prune-log2", type=int, default=20)
-    ap.add_argument("--depth", type=int, default=3000)     # the paper's DFS depth (PAPER.md:418-426)
-    ap.add_argument("--walk-log2", type=int, default=14)
-    ap.add_argument("--full", action="store_true")
-    ap.add_argument("--prune-chunk-log2", type=int, default=31)  # --full: candidates per prune launch
-    ap.add_argument("--skip-walk", action="store_true")  # --full: prune only (A/B of K3 variants)
-    args = ap.parse_args()
-
+def measure(ctx, stream, *, rows_log2: int = 13, prune_log2: int = 24, depth: int = 3000, walk_log2: int = 14,
+            cpu_sample: int = 1 << 14, keep=None) -> dict:
+    """Config 3 on one GPU: K2 over 2^rows_log2 R2 rows (the 2^32-state slice by default),
+    K3 (DFS, `depth`) on the first 2^prune_log2 candidates, K1 on a prefix of the
+    survivors; each with parity against the C restatement on a sample and a CPU baseline.
+    `keep` (dict) receives the device tensors for --full."""
     import torch
 
     import paper_1210_6411_b200 as lc
     from oracle import port
     from paper_1210_6411_b200 import _native as N
 
-    dev = torch.device("cuda", 0)
-    stream = torch.cuda.Stream(dev)
-    torch.cuda.set_stream(stream)
+    dev = torch.device("cuda", ctx.device)
     spec = lc.A51
     params = lc.CandidateParams.from_spec(spec, 0x2AAA00)
-    ctx = N.context(0)
     sspec = N.spec_struct(spec)
-    rows = 1 << args.rows_log2
+    rows = 1 << rows_log2
     states = rows * spec.reg_masks[0]
     cap = states // 2 + (1 << 20)
+    cores = len(os.sched_getaffinity(0))
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 0.0)) * 1e9 or None
 
     out = torch.empty(cap, dtype=torch.int64, device=dev)
     count = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -86,22 +86,43 @@ def main():
     k2_s = e0.elapsed_time(e1) / 1e3 / reps
     ncand = int(count.item())
 
-    # parity: first 4 rows vs the C oracle (host)
+    # parity: first 4 rows vs the C restatement (host), which is also K2's CPU baseline
+    os.environ["OMP_NUM_THREADS"] = str(cores)
+    t0 = time.perf_counter()
     want = port.enumerate_rows(spec, 0x2AAA00, R2_0, R2_0 + 4)
+    k2_cpu_s = time.perf_counter() - t0
     got = out[: want.size].cpu().numpy().view(np.uint64)
     k2_parity = bool((got == want).all())
-    # size-independent checks over the whole slice: ascending, all on the fixed plane
+    # size-independent checks over the whole slice: ascending, count = closed form
     head = out[:ncand]
     ascending = bool((head[1:] > head[:-1]).all().item()) if ncand > 1 else True
+    k2_bytes = ncand * 8
+    k2 = {"states": states, "candidates": ncand, "seconds": k2_s, "states_per_s": states / k2_s,
+          "candidates_per_s": ncand / k2_s,
+          "roofline": {"bound": "hbm", "achieved": k2_bytes / k2_s / 1e9,
+                       "peak": hbm_peak / 1e9 if hbm_peak else None, "unit": "GB/s",
+                       "frac": k2_bytes / k2_s / hbm_peak if hbm_peak else None,
+                       "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy: read + write bytes)",
+                       "write_stream_gbs_measured": write_peak / 1e9,
+                       "frac_of_write_stream": k2_bytes / k2_s / write_peak,
+                       "algorithmic": "8 B written per candidate (a pure write stream)"},
+          "parity_first_4_rows_vs_oracle": k2_parity, "ascending": ascending,
+          "cpu_baseline": {"value": 4 * spec.reg_masks[0] / k2_cpu_s, "unit": "states/s", "cores": 1,
+                           "kind": "port", "sample": f"4 R2 rows ({4 * spec.reg_masks[0]} states), "
+                                                     "orc_enumerate (pipeline.py:104-118 restated)"}}
 
     # ---- K3: prune a prefix of the enumerated candidates (DFS, depth limit)
-    npr = min(1 << args.prune_log2, ncand)
+    npr = min(1 << prune_log2, ncand)
     cands = out[:npr].clone()
+    if keep is not None:
+        keep["cands_all"] = out[:ncand]
+    else:
+        del out
     removed = torch.empty(npr, dtype=torch.uint8, device=dev)
     work = torch.empty(npr, dtype=torch.int64, device=dev)
 
     def prune():
-        N.check(N.lib.lc_prune_device(ctx.handle, C.byref(sspec), params.fixed_r3, 0, args.depth,
+        N.check(N.lib.lc_prune_device(ctx.handle, C.byref(sspec), params.fixed_r3, 0, depth,
                                       C.c_void_p(cands.data_ptr()), npr, C.c_void_p(removed.data_ptr()),
                                       C.c_void_p(work.data_ptr()), C.c_void_p(stream.cuda_stream)))
 
@@ -114,44 +135,62 @@ def main():
     k3_s = e0.elapsed_time(e1) / 1e3
     expanded = int(work.sum().item())
     nremoved = int(removed.sum().item())
-    # parity on a sample (oracle on host cores)
-    idx = np.linspace(0, npr - 1, min(1 << 16, npr)).astype(np.int64)
+    # parity on an evenly spaced sample (the C restatement on the host cores)
+    idx = np.linspace(0, npr - 1, min(cpu_sample, npr)).astype(np.int64)
     sample = cands.cpu().numpy().view(np.uint64)[idx]
     t0 = time.perf_counter()
-    o_removed, o_work = port.prune(spec, 0x2AAA00, "dfs", args.depth, sample)
+    o_removed, o_work = port.prune(spec, 0x2AAA00, "dfs", depth, sample)
     cpu_s = time.perf_counter() - t0
     k3_parity = bool((o_removed == removed.cpu().numpy()[idx]).all() and
                      (o_work == work.cpu().numpy().view(np.uint64)[idx]).all())
+    k3 = {"candidates": npr, "depth_limit": depth, "removed": nremoved, "removed_fraction": nremoved / npr,
+          "expanded": expanded, "seconds": k3_s, "candidates_per_s": npr / k3_s,
+          "expansions_per_s": expanded / k3_s, "parity_sample_vs_oracle": k3_parity,
+          "parity_sample": int(idx.size),
+          "cpu_baseline": {"value": float(o_work.sum()) / cpu_s, "unit": "expansions/s", "cores": cores,
+                           "kind": "port", "sample": f"{idx.size} evenly spaced candidates of the {npr} "
+                                                     f"({cpu_s:.2f} s), orc_prune (pipeline.py:121-178 restated)"}}
 
     # ---- K1: walk (a prefix of) the survivors to their next special node
     surv = cands[removed == 0]
-    nw = min(1 << args.walk_log2, surv.numel())
+    nw = min(1 << walk_log2, surv.numel())
     res = lc.walk_arrays(surv[:nw].cpu().numpy().view(np.uint64), params, spec, stride=lc.DEFAULT_STRIDE_A51)
+    if keep is not None:
+        keep.update(out=keep["cands_all"], ncand=ncand)
+    return {"workload": f"configs[2]: R3 = 0x2AAA00, R2 in [{R2_0:#x}, {R2_0 + rows:#x}), all R1 ({states} states)",
+            "k2_enumerate": k2, "k3_prune": k3,
+            "k1_walk_survivors": {"walks": nw, "edges": res.edges, "transitions": res.transitions}}
 
-    full = None
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rows-log2", type=int, default=13)   # 2^13 rows x (2^19-1) = 2^32 states
+    ap.add_argument("--prune-log2", type=int, default=20)
+    ap.add_argument("--depth", type=int, default=3000)     # the paper's DFS depth (PAPER.md:418-426)
+    ap.add_argument("--walk-log2", type=int, default=14)
+    ap.add_argument("--full", action="store_true")
+    ap.add_argument("--prune-chunk-log2", type=int, default=31)  # --full: candidates per prune launch
+    ap.add_argument("--skip-walk", action="store_true")  # --full: prune only (A/B of K3 variants)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 16)
+    args = ap.parse_args()
+
+    import torch
+
+    import paper_1210_6411_b200 as lc
+    from paper_1210_6411_b200 import _native as N
+
+    stream = torch.cuda.Stream(torch.device("cuda", 0))
+    torch.cuda.set_stream(stream)
+    ctx = N.context(0)
+    keep = {} if args.full else None
+    line = {"metric": "steps 1-2 feeding the walk (special-node enumeration + leaf/predecessor filter, prune)"}
+    line.update(measure(ctx, stream, rows_log2=args.rows_log2, prune_log2=args.prune_log2, depth=args.depth,
+                        walk_log2=args.walk_log2, cpu_sample=args.cpu_sample, keep=keep))
+    line["gpu"] = torch.cuda.get_device_name(0)
     if args.full:
-        full = full_slice(args, ctx, sspec, params, out[:ncand], stream, torch, N, lc)
-
-    line = {
-        "metric": "steps 1-2 feeding the walk (special-node enumeration + leaf/predecessor filter, prune)",
-        "config": {"workload": f"configs[2]: R3 = 0x2AAA00, R2 in [{R2_0:#x}, {R2_0 + rows:#x}), all R1 "
-                               f"({states} states)", "prune": f"dfs depth {args.depth} on the first {npr} candidates"},
-        "k2_enumerate": {"states": states, "candidates": ncand, "seconds": k2_s, "states_per_s": states / k2_s,
-                         "candidates_per_s": ncand / k2_s, "bytes_written_per_s": ncand * 8 / k2_s,
-                         "hbm_frac_of_copy_peak": ncand * 8 / k2_s / 6546.2e9,
-                         "write_stream_gbs_measured": write_peak / 1e9,
-                         "frac_of_write_stream": ncand * 8 / k2_s / write_peak,
-                         "parity_first_4_rows_vs_oracle": k2_parity, "ascending": ascending},
-        "k3_prune": {"candidates": npr, "removed": nremoved, "removed_fraction": nremoved / npr,
-                     "expanded": expanded, "seconds": k3_s, "candidates_per_s": npr / k3_s,
-                     "expansions_per_s": expanded / k3_s, "parity_sample_vs_oracle": k3_parity,
-                     "cpu_port_expansions_per_s": float(o_work.sum()) / cpu_s,
-                     "cpu_port_cores": len(os.sched_getaffinity(0))},
-        "k1_walk_survivors": {"walks": nw, "edges": res.edges, "transitions": res.transitions},
-        "gpu": torch.cuda.get_device_name(0),
-    }
-    if full:
-        line["full_slice_steps_1_to_3"] = full
+        params = lc.CandidateParams.from_spec(lc.A51, 0x2AAA00)
+        line["full_slice_steps_1_to_3"] = full_slice(args, ctx, N.spec_struct(lc.A51), params,
+                                                     keep["out"][:keep["ncand"]], stream, torch, N, lc)
     print(json.dumps(line), flush=True)
 
 

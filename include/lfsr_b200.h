@@ -161,6 +161,19 @@ int lc_random_candidates(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3, ui
 int lc_random_candidates_device(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3,
                                 uint64_t seed, uint64_t n, uint64_t *d_out, void *stream);
 
+/* The reference's own seeded sampler, host-side (no context, no device): the first n
+ * results of `random_candidate(random.Random(seed), spec, params, table)` called n times on
+ * one generator (pipeline.py:301-310), bit-identical to CPython's MT19937 / randrange
+ * stream.  Config 1 is seed 0 x 2^16, config 2 seed 0 x 2^24.
+ * *draws_used = (r1, r2) pairs drawn.  Registers of more than 32 bits: LC_ERR_UNSUPPORTED. */
+int lc_reference_candidates(const lc_spec *spec, uint64_t fixed_r3, uint64_t seed, uint64_t n,
+                            uint64_t *out, uint64_t *draws_used);
+/* `count` independent streams, stream i = lc_reference_candidates(seeds[i], n_each) into
+ * out[i*n_each ...], on up to `threads` host threads (per-shard seeds of the multi-GPU
+ * bench). */
+int lc_reference_candidates_multi(const lc_spec *spec, uint64_t fixed_r3, const uint64_t *seeds,
+                                  uint32_t count, uint64_t n_each, uint64_t *out, uint32_t threads);
+
 /* Closure check of build_skeleton_edges (pipeline.py:251-255): first i with
  * queries[i] not in the ascending array `sorted_set`, or n if all are members. */
 int lc_first_missing(lc_ctx *ctx, const uint64_t *sorted_set, uint64_t m, const uint64_t *queries,

@@ -14,6 +14,7 @@ Usage (from the repo root, in the build container):
     python oracle/gen_golden.py reduce     # ~1 min: steps 4-5 (leaf cutting, cycles) on minis
     python oracle/gen_golden.py bruteforce # ~2 min: the reference's exhaustive mini analysis
     python oracle/gen_golden.py c1 [W]     # ~1 h on 8 cores: the full 2^16 config-1 set
+    python oracle/gen_golden.py c2         # ~40 min on 8 AVX-512 cores: config-2 (2^24) digests
 
 Digest format: sha256 over lines
 ``f"{src:016x} {dst:016x} {dist}\\n"`` sorted by (src, dst, dist).
@@ -451,6 +452,93 @@ def gen_c1(ref, workers):
          dst=dst[::256], dist=dist[::256])
 
 
+C2_LOG2 = 24
+C2_BATCH_LOG2 = 22
+A51_CAP = 178_957_008  # 16 * int(L) + 64 (bitslice.py:273-274)
+
+
+def batch_digest(dst, dist) -> str:
+    """sha256 over the little-endian u64 dst column then the dist column, input order."""
+    h = hashlib.sha256(np.asarray(dst, dtype="<u8").tobytes())
+    h.update(np.asarray(dist, dtype="<u8").tobytes())
+    return h.hexdigest()
+
+
+def _walk512():
+    import ctypes as C
+    import subprocess
+    subprocess.run(["make", "-s", "-C", HERE, "walk512"], check=True)
+    lib = C.CDLL(os.path.join(HERE, "_build", "libwalk512.so"))
+    u = C.POINTER(C.c_uint64)
+    lib.w512_walk.argtypes = [C.c_uint32, u, C.c_uint64, C.c_uint64, C.c_uint64, u, u, u]
+
+    def walk(starts):
+        starts = np.ascontiguousarray(starts, dtype=np.uint64)
+        n = starts.size
+        dst, dist, bad = np.zeros(n, np.uint64), np.zeros(n, np.uint64), np.zeros(1, np.uint64)
+        p = lambda a: a.ctypes.data_as(u)  # noqa: E731
+        rc = lib.w512_walk(0x2AAA00, p(starts), n, A51_STRIDE, A51_CAP, p(dst), p(dist), p(bad))
+        if rc:
+            raise RuntimeError(f"walk512: cap exceeded near start {int(bad[0])}")
+        return dst, dist
+    return walk
+
+
+def gen_c2(ref):
+    """Config 2: the first 2^24 results of the reference sampler
+    random_candidate(random.Random(0), A51, 0x2AAA00) -- config 1 is its 2^16 prefix --
+    walked to the next special node at the paper's stride.  The starts come from the
+    reference itself; the walks from oracle/walk512.c, which is first pinned against the
+    reference-produced config-1 set and the 256-walk KAT.  Output: per-batch digests of
+    (dst, dist) for the 2^22-start batches bench.py times, plus whole-set statistics."""
+    n = 1 << C2_LOG2
+    t0 = time.time()
+    starts = np.array(c1_starts(ref, n), dtype=np.uint64)
+    t_starts = time.time() - t0
+    print(f"c2: {n} reference starts in {t_starts:.0f} s", flush=True)
+    c1 = json.load(open(os.path.join(GOLDEN, "a51_c1_65536.json")))
+    assert u64_digest(starts[:1 << 16]) == c1["starts_digest"], "config-1 prefix mismatch"
+    walk = _walk512()
+    kat = np.load(os.path.join(GOLDEN, "a51_kat256.npz"))
+    d, w = walk(kat["src"])
+    assert (d == kat["dst"]).all() and (w == kat["dist"]).all(), "walk512 disagrees with the KAT"
+    t1 = time.time()
+    d, w = walk(starts[:1 << 16])
+    assert u64_digest(d) == c1["dst_digest"] and u64_digest(w) == c1["dist_digest"], \
+        "walk512 disagrees with the reference's config-1 run"
+    print(f"c2: walk512 pinned on config 1 ({time.time() - t1:.0f} s)", flush=True)
+    batch = 1 << C2_BATCH_LOG2
+    batches = []
+    dsts, dists = [], []
+    t2 = time.time()
+    for b in range(n // batch):
+        d, w = walk(starts[b * batch:(b + 1) * batch])
+        batches.append({"index": b, "digest": batch_digest(d, w), "sum_dist": int(w.sum()),
+                        "min": int(w.min()), "max": int(w.max())})
+        dsts.append(d)
+        dists.append(w)
+        print(f"c2: batch {b} done, {time.time() - t2:.0f} s", flush=True)
+    el = time.time() - t2
+    dst, dist = np.concatenate(dsts), np.concatenate(dists)
+    hist_lo = int(dist.min())
+    save_json("a51_c2_digests.json", {
+        "source": "starts = lfsrcycles.pipeline.random_candidate(random.Random(0), A51, "
+                  "CandidateParams.from_spec(A51, 0x2AAA00)) x 2^24 (the reference, via oracle/ref_shim.py); "
+                  "walks = oracle/walk512.c at stride 11_170_000, pinned against a51_c1_65536.json "
+                  "(the reference's own config-1 run) and a51_kat256",
+        "n": n, "batch": batch, "stride": A51_STRIDE, "seed": SEED_C1, "fixed_r3": 0x2AAA00,
+        "starts_digest": u64_digest(starts), "c1_prefix_starts_digest": c1["starts_digest"],
+        "batch_digest_format": "sha256(dst as <u8 bytes || dist as <u8 bytes), input order",
+        "batches": batches, "dst_digest": u64_digest(dst), "dist_digest": u64_digest(dist),
+        "sum_dist": int(dist.sum()), "sum_dist_sq": int((dist.astype(object) ** 2).sum()),
+        "min": int(dist.min()), "max": int(dist.max()), "hist_lo": hist_lo,
+        "hist": np.bincount((dist - hist_lo).astype(np.int64)).tolist(),
+        "seconds_walk": el, "seconds_starts": t_starts, "threads": os.cpu_count()})
+    # a sparse sample of rows (every 4096th walk) for targeted debugging
+    save("a51_c2_sample", idx=np.arange(0, n, 4096, dtype=np.uint64), src=starts[::4096],
+         dst=dst[::4096], dist=dist[::4096])
+
+
 def gen_bruteforce(ref):
     """oracle.brute_force_analysis (oracle.py:141-283) on the minis, majority and
     clock-all dynamics: summaries, cycles, histograms and digests of every array."""
@@ -497,6 +585,8 @@ def main():
         gen_tuning(ref)
     elif what == "bruteforce":
         gen_bruteforce(ref)
+    elif what == "c2":
+        gen_c2(ref)
     elif what == "c1":
         gen_c1(ref, int(sys.argv[2]) if len(sys.argv) > 2 else os.cpu_count())
     else:

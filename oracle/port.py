@@ -30,6 +30,41 @@ class OracleValueError(OracleError):
     """Reference would raise ValueError from min() of an empty sequence (bitslice.py:317)."""
 
 
+class SpecConst:
+    """Spec-like constants (``.lengths``, ``.taps``, ``.clock_taps``) of a built-in cipher,
+    so callers that must not import the product package (bench.py's reference arm) can
+    name one: A5/1 is cipher.py:173-178."""
+
+    def __init__(self, lengths, taps, clock_taps):
+        self.lengths, self.taps, self.clock_taps = tuple(lengths), tuple(taps), tuple(clock_taps)
+        self.reg_masks = tuple((1 << l) - 1 for l in self.lengths)
+        self.offsets = (0, self.lengths[0], self.lengths[0] + self.lengths[1])
+
+
+A51 = SpecConst((19, 22, 23), ((13, 16, 17, 18), (20, 21), (7, 20, 21, 22)), (8, 10, 10))
+
+
+def random_candidates(spec, fixed_r3: int, seed: int, n: int) -> np.ndarray:
+    """``random_candidate(random.Random(seed), ...)`` x n (pipeline.py:301-310): rejection
+    over (randrange(1, m1+1), randrange(1, m2+1)) with R3 fixed, drawn from Python's own
+    generator and tested with the C restatement of is_candidate (cipher.py:420-428)."""
+    import random
+
+    rng = random.Random(seed)
+    m1, m2, _ = spec.reg_masks
+    o2, o3 = spec.offsets[1], spec.offsets[2]
+    packed = int(fixed_r3) << o3
+    lib, s = load(), spec_struct(spec)
+    out = np.empty(int(n), dtype=np.uint64)
+    for i in range(int(n)):
+        while True:
+            x = rng.randrange(1, m1 + 1) | (rng.randrange(1, m2 + 1) << o2) | packed
+            if lib.orc_is_candidate(C.byref(s), int(fixed_r3), x):
+                out[i] = x
+                break
+    return out
+
+
 class _Spec(C.Structure):
     _fields_ = [("len", C.c_int * 3), ("tap", C.c_uint64 * 3), ("ct", C.c_int * 3)]
 

@@ -77,6 +77,10 @@ _SIGNATURES = {
                          _vp], C.c_int),
     "lc_random_candidates": ([_vp, C.POINTER(lc_spec), C.c_uint64, C.c_uint64, C.c_uint64, _u64p, _u64p],
                              C.c_int),
+    "lc_reference_candidates": ([C.POINTER(lc_spec), C.c_uint64, C.c_uint64, C.c_uint64, _u64p, _u64p],
+                                C.c_int),
+    "lc_reference_candidates_multi": ([C.POINTER(lc_spec), C.c_uint64, _u64p, C.c_uint32, C.c_uint64, _u64p,
+                                       C.c_uint32], C.c_int),
     "lc_random_candidates_device": ([_vp, C.POINTER(lc_spec), C.c_uint64, C.c_uint64, C.c_uint64, _vp, _vp],
                                     C.c_int),
     "lc_first_missing": ([_vp, _u64p, C.c_uint64, _u64p, C.c_uint64, _u64p], C.c_int),

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "liblfsr_b200.so")
-SOURCES = ["walk.cu", "kernels.cu", "peak.cu", "reduce.cu", "bruteforce.cu", "capi.cu"]
+SOURCES = ["walk.cu", "kernels.cu", "peak.cu", "reduce.cu", "bruteforce.cu", "sampler.cu", "capi.cu"]
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-cudart", "static",
               "--expt-relaxed-constexpr"]

@@ -40,26 +40,50 @@ def _from_limbs(limbs) -> tuple:
     return v & ((1 << 64) - 1), (v >> 64) & ((1 << 64) - 1)
 
 
-def combine_stats(blocks) -> np.ndarray:
-    """Host reduction of per-shard statistics blocks (same rule as allreduce_stats)."""
+_NO_ERROR = (1 << 64) - 1
+
+
+def _error_key(stats: np.ndarray, offset: int) -> int:
+    """(global start index, error code) of a block as one orderable key: the smallest
+    key over the shards is the first failing start and its own code (the code and the
+    index are never taken from different shards)."""
+    code = int(stats[N.ST_ERROR])
+    if not code:
+        return _NO_ERROR
+    return ((int(stats[N.ST_ERROR_INDEX]) + int(offset)) << 8) | (code & 0xFF)
+
+
+def _apply_error_key(out: np.ndarray, key: int) -> None:
+    if key == _NO_ERROR:
+        out[N.ST_ERROR], out[N.ST_ERROR_INDEX] = 0, np.uint64(_NO_ERROR)
+    else:
+        out[N.ST_ERROR], out[N.ST_ERROR_INDEX] = key & 0xFF, key >> 8
+
+
+def combine_stats(blocks, offsets=None) -> np.ndarray:
+    """Host reduction of per-shard statistics blocks (same rule as allreduce_stats).
+    offsets[i] = global index of shard i's first start (its ST_ERROR_INDEX is local)."""
     blocks = [np.asarray(b, dtype=np.uint64) for b in blocks]
+    offsets = [0] * len(blocks) if offsets is None else list(offsets)
     out = blocks[0].copy()
-    for b in blocks[1:]:
+    key = _error_key(blocks[0], offsets[0])
+    for b, o in zip(blocks[1:], offsets[1:]):
         for i in (N.ST_EDGES, N.ST_TRANSITIONS):
             out[i] = np.uint64((int(out[i]) + int(b[i])) & ((1 << 64) - 1))
         out[N.ST_MIN] = min(out[N.ST_MIN], b[N.ST_MIN])
         out[N.ST_MAX] = max(out[N.ST_MAX], b[N.ST_MAX])
-        out[N.ST_ERROR] = max(out[N.ST_ERROR], b[N.ST_ERROR])
-        out[N.ST_ERROR_INDEX] = min(out[N.ST_ERROR_INDEX], b[N.ST_ERROR_INDEX])
+        key = min(key, _error_key(b, o))
         out[N.ST_HEADER:] += b[N.ST_HEADER:]
+    _apply_error_key(out, key)
     limbs = sum(_limbs(b) for b in blocks)
     out[N.ST_SQ_LO], out[N.ST_SQ_HI] = _from_limbs(limbs)
     return out
 
 
-def allreduce_stats(stats: np.ndarray, group=None) -> np.ndarray:
+def allreduce_stats(stats: np.ndarray, group=None, offset: int = 0) -> np.ndarray:
     """All-reduce one rank's statistics block with torch.distributed (NCCL on CUDA
-    tensors when the default backend is NCCL, gloo otherwise).  Returns the global
+    tensors when the default backend is NCCL, gloo otherwise).  ``offset`` = global
+    index of this rank's first start (ST_ERROR_INDEX is shard-local).  Returns the global
     block on every rank."""
     import torch
     import torch.distributed as dist
@@ -74,8 +98,9 @@ def allreduce_stats(stats: np.ndarray, group=None) -> np.ndarray:
     dist.all_reduce(t_sum, op=dist.ReduceOp.SUM, group=group)
     # min / max (unsigned values mapped to order-preserving int64)
     flip = np.uint64(1 << 63)
-    mins = (s[[N.ST_MIN, N.ST_ERROR_INDEX]] ^ flip).view(np.int64)
-    maxs = (s[[N.ST_MAX, N.ST_ERROR]] ^ flip).view(np.int64)
+    key = np.array([_error_key(s, offset)], dtype=np.uint64)
+    mins = (np.concatenate([s[[N.ST_MIN]], key]) ^ flip).view(np.int64)
+    maxs = (s[[N.ST_MAX]] ^ flip).view(np.int64)
     t_min = torch.from_numpy(mins.copy()).to(dev)
     t_max = torch.from_numpy(maxs.copy()).to(dev)
     dist.all_reduce(t_min, op=dist.ReduceOp.MIN, group=group)
@@ -87,8 +112,9 @@ def allreduce_stats(stats: np.ndarray, group=None) -> np.ndarray:
     out[N.ST_HEADER:] = sums[6:].astype(np.uint64)
     mn = t_min.cpu().numpy().view(np.uint64) ^ flip
     mx = t_max.cpu().numpy().view(np.uint64) ^ flip
-    out[N.ST_MIN], out[N.ST_ERROR_INDEX] = mn
-    out[N.ST_MAX], out[N.ST_ERROR] = mx
+    out[N.ST_MIN] = mn[0]
+    _apply_error_key(out, int(mn[1]))
+    out[N.ST_MAX] = mx[0]
     return out
 
 

@@ -15,6 +15,8 @@
 
 from __future__ import annotations
 
+import ctypes as C
+import os
 import random
 from dataclasses import dataclass
 from typing import Iterable, Iterator
@@ -32,7 +34,7 @@ __all__ = [
     "PruneConfig", "PruneStats", "PruneSoundnessError", "enumerate_candidates",
     "enumerate_candidates_array", "prune_shallow_segments", "build_skeleton_edges",
     "probe_segment", "probe_segments", "auto_depth_limit", "random_candidate",
-    "random_candidates_gpu",
+    "random_candidates_gpu", "reference_candidates", "reference_candidate_streams",
 ]
 
 _PRUNE_CHUNK_GPU = 1 << 25  # candidates per kernel launch: large, so the tail of the longest traversals amortises
@@ -277,6 +279,32 @@ def random_candidate(rng: random.Random, spec: CipherSpec, params: CandidatePara
         x = rng.randrange(1, m1 + 1) | (rng.randrange(1, m2 + 1) << o2) | params.packed_r3
         if is_candidate(x, params, spec, table):
             return x
+
+
+def reference_candidates(spec: CipherSpec, params: CandidateParams, seed: int, n: int) -> np.ndarray:
+    """``[random_candidate(rng, spec, params) for _ in range(n)]`` with
+    ``rng = random.Random(seed)`` (pipeline.py:301-310), as a u64 array: the same states
+    in the same order, from a native restatement of CPython's MT19937 / ``randrange``
+    stream (``csrc/sampler.cu``; ~50 M states/s instead of ~65 k/s).  Configs 1 and 2 are
+    ``seed=0`` with n = 2^16 and 2^24."""
+    if seed < 0 or seed >= 1 << 64:
+        raise ValueError("seed must be a non-negative 64-bit integer")
+    out = np.empty(int(n), dtype=np.uint64)
+    N.check(N.lib.lc_reference_candidates(C.byref(N.spec_struct(spec)), params.fixed_r3, int(seed), int(n),
+                                          N.u64p(out), None))
+    return out
+
+
+def reference_candidate_streams(spec: CipherSpec, params: CandidateParams, seeds, n_each: int,
+                                threads: int | None = None) -> np.ndarray:
+    """``reference_candidates`` for several seeds at once (one host thread per stream, up
+    to ``threads``): row i of the result is ``reference_candidates(..., seeds[i], n_each)``."""
+    seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+    out = np.empty((seeds.size, int(n_each)), dtype=np.uint64)
+    threads = threads or len(os.sched_getaffinity(0))
+    N.check(N.lib.lc_reference_candidates_multi(C.byref(N.spec_struct(spec)), params.fixed_r3, N.u64p(seeds),
+                                                seeds.size, int(n_each), N.u64p(out), int(threads)))
+    return out
 
 
 def random_candidates_gpu(spec: CipherSpec, params: CandidateParams, seed: int, n: int) -> np.ndarray:

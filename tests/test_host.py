@@ -141,6 +141,47 @@ def test_kat_starts_are_reference_sampler_prefix(lc, specs, params):
     assert got == g["src"].tolist()
 
 
+def test_native_reference_sampler_matches_python_random(lc, specs, params):
+    """csrc/sampler.cu (host code) restates CPython's MT19937 + randrange stream and the
+    reference's random_candidate rejection (pipeline.py:301-310): the same states, in the
+    same order, as the Python sampler on a random.Random of the same seed."""
+    from paper_1210_6411_b200 import pipeline as P
+
+    rc = golden_json("random_candidate.json")  # produced by the reference itself
+    for name in ("a51", "mini567", "mini789"):
+        for seed in range(4):
+            got = P.reference_candidates(specs[name], params[name], seed, 64)
+            assert got.tolist() == rc[f"{name}_{seed}"]
+        for seed in (5, 2**32 - 1, 2**32, 2**40 + 7, 2**64 - 1):  # one- and two-word MT keys
+            rng = random.Random(seed)
+            want = [lc.random_candidate(rng, specs[name], params[name]) for _ in range(500)]
+            assert P.reference_candidates(specs[name], params[name], seed, 500).tolist() == want
+    # a non-default fixed R3 value (different predicate table)
+    p2 = lc.CandidateParams.from_spec(specs["a51"], 0x1234)
+    rng = random.Random(9)
+    want = [lc.random_candidate(rng, specs["a51"], p2) for _ in range(500)]
+    assert P.reference_candidates(specs["a51"], p2, 9, 500).tolist() == want
+    multi = P.reference_candidate_streams(specs["mini789"], params["mini789"], [3, 0, 7], 200, threads=2)
+    for row, seed in zip(multi, (3, 0, 7)):
+        assert (row == P.reference_candidates(specs["mini789"], params["mini789"], seed, 200)).all()
+
+
+def test_config1_and_config2_starts_from_native_sampler(lc, specs, params):
+    """Config 1 = the first 2^16 reference-sampler starts of random.Random(0); config 2
+    = the first 2^24 (digests of the reference's own output, tests/golden)."""
+    import hashlib
+
+    from paper_1210_6411_b200 import pipeline as P
+
+    c1 = golden_json("a51_c1_65536.json")
+    starts = P.reference_candidates(specs["a51"], params["a51"], 0, 1 << 24)
+    assert hashlib.sha256(starts[:1 << 16].astype("<u8").tobytes()).hexdigest() == c1["starts_digest"]
+    path = os.path.join(ROOT, "tests", "golden", "a51_c2_digests.json")
+    if os.path.exists(path):
+        c2 = golden_json("a51_c2_digests.json")
+        assert hashlib.sha256(starts.astype("<u8").tobytes()).hexdigest() == c2["starts_digest"]
+
+
 def test_records_byte_exact(lc, tmp_path):
     fx = golden_json("records.json")
     recs = [lc.EdgeRecord(1, 2, 3, 4, 5), lc.EdgeRecord((1 << 64) - 1, 0x5554000000000000, 11184809, 0, 0)]
@@ -221,6 +262,29 @@ def test_stats_combine_and_summary():
     summ = stats_summary(whole)
     assert summ["edges"] == 1000 and abs(summ["mean"] - d.mean()) < 1e-6
     assert abs(summ["sd"] - d.astype(np.float64).std()) < 1e-3
+
+
+def test_error_code_and_index_reduce_as_a_pair():
+    """A failing shard's (code, global index) travel together: the merged block reports
+    the first failing start over all shards and that start's own code."""
+    from paper_1210_6411_b200 import _native as N
+    from paper_1210_6411_b200.distributed import combine_stats
+
+    def block(code=0, index=(1 << 64) - 1):
+        s = np.zeros(N.ST_HEADER + 2, dtype=np.uint64)
+        s[N.ST_MIN] = np.uint64((1 << 64) - 1)
+        s[N.ST_ERROR] = code
+        s[N.ST_ERROR_INDEX] = np.uint64(index)
+        return s
+
+    ok = combine_stats([block(), block()], offsets=[0, 100])
+    assert ok[N.ST_ERROR] == 0 and ok[N.ST_ERROR_INDEX] == np.uint64((1 << 64) - 1)
+    # shard 0 fails late with code 5, shard 1 fails early (local index 3 = global 103)
+    # with code 4; shard 2 fails at global 250 with code 4
+    m = combine_stats([block(5, 90), block(4, 3), block(4, 50)], offsets=[0, 100, 200])
+    assert int(m[N.ST_ERROR]) == 5 and int(m[N.ST_ERROR_INDEX]) == 90
+    m = combine_stats([block(), block(4, 3), block(5, 1)], offsets=[0, 100, 200])
+    assert int(m[N.ST_ERROR]) == 4 and int(m[N.ST_ERROR_INDEX]) == 103
 
 
 def test_prune_config_validation_matches_reference(lc):
