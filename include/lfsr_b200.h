@@ -14,6 +14,10 @@
  *    a cudaStream_t (passed as void*), enqueue work and return without synchronising.
  *  - Return 0 on success or a negative LC_ERR_* code; lc_last_error() (thread-local)
  *    holds the message.  No C++ exception crosses the ABI.
+ *  - A context owns scratch buffers (walk pools, queues, staging).  Calls on one context
+ *    are ordered on the device: each call's stream first waits for the previous call's
+ *    work (an event the context records), so `_device` calls on different streams may
+ *    share a context safely; they then run one after another, not concurrently.
  *  - Only the three built-in ciphers (A5/1, mini567, mini789 -- cipher.py:173-194) have
  *    compiled kernels; any other spec returns LC_ERR_UNSUPPORTED (there is no CPU path).
  */
@@ -186,6 +190,13 @@ int lc_first_missing(lc_ctx *ctx, const uint64_t *sorted_set, uint64_t m, const 
  * and step 4 require (records.py:3-5, reduce.py:3-4). */
 int lc_sort_edges(lc_ctx *ctx, uint64_t n, uint64_t *src, uint64_t *dst, uint64_t *dist,
                   uint64_t *subtree_size, uint64_t *subtree_depth);
+/* Device form, out of place: d_in[0..4] = (source, destination, distance, subtree_size,
+ * subtree_depth) columns (sizes / depths may be NULL), d_out[0..4] receive them sorted by
+ * source (stable: equal sources keep their input order).  The output columns must not
+ * alias the inputs; n < 2^32.  Enqueued on `stream` without a host synchronisation
+ * (in-house LSD radix sort, csrc/sort.cu). */
+int lc_sort_edges_device(lc_ctx *ctx, uint64_t n, const uint64_t *const *d_in, uint64_t *const *d_out,
+                         void *stream);
 
 /* Edge-output writer: 40-byte little-endian '<5Q' records (records.py:24-36) from
  * device columns, d_out = 5 * n u64 words (subtree_size / subtree_depth may be NULL:

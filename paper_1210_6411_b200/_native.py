@@ -85,6 +85,7 @@ _SIGNATURES = {
                                     C.c_int),
     "lc_first_missing": ([_vp, _u64p, C.c_uint64, _u64p, C.c_uint64, _u64p], C.c_int),
     "lc_sort_edges": ([_vp, C.c_uint64, _u64p, _u64p, _u64p, _u64p, _u64p], C.c_int),
+    "lc_sort_edges_device": ([_vp, C.c_uint64, C.POINTER(_vp), C.POINTER(_vp), _vp], C.c_int),
     "lc_pack_records_device": ([_vp, C.c_uint64, _vp, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "lc_cut_leaves": ([_vp, C.c_uint64, _u64p, _u64p, _u64p, _u64p, _u64p, C.c_uint32, _u64p, C.c_uint32,
                        C.POINTER(C.c_uint32), _u64p], C.c_int),

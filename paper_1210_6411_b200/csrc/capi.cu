@@ -121,9 +121,22 @@ struct lc_ctx {
   int mapped_sms = -1;  // SMs found by the %smid probe (-1: not probed yet)
   int need3_id = -1;    // spec / fixed R3 the need3 table was built for
   uint64_t need3_f = 0;
+  cudaEvent_t done = nullptr;  // recorded after the last call's work (see Ordered)
 };
 
 namespace {
+
+// Every call that uses the context's scratch buffers (walk pools, queues, lane metadata,
+// staging) first makes its stream wait for the previous call's work, on whatever stream
+// that was, and records its own completion: asynchronous `_device` calls on different
+// streams can then share one context without one call's rounds overwriting another's
+// buffers.
+struct Ordered {
+  lc_ctx* c;
+  cudaStream_t st;
+  Ordered(lc_ctx* c_, cudaStream_t st_) : c(c_), st(st_) { cudaStreamWaitEvent(st, c->done, 0); }
+  ~Ordered() { cudaEventRecord(c->done, st); }
+};
 
 // Dense index for every %smid of the device, so the walk can keep one queue per warp
 // scheduler (4 per SM).  Probed once per context.
@@ -200,6 +213,8 @@ int lc_ctx_create(int device, lc_ctx** out) {
   c->device = device;
   cudaError_t e = cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(c->done, c->stream);
   if (e != cudaSuccess) {
     delete c;
     return fail(LC_ERR_CUDA, "context: %s", cudaGetErrorString(e));
@@ -211,10 +226,11 @@ int lc_ctx_create(int device, lc_ctx** out) {
 int lc_ctx_destroy(lc_ctx* ctx) {
   if (!ctx) return LC_OK;
   cudaSetDevice(ctx->device);
-  cudaStreamSynchronize(ctx->stream);
+  cudaDeviceSynchronize();  // work queued on callers' streams may still use the buffers
   for (DevBuf* b : {&ctx->meta, &ctx->queue, &ctx->stats, &ctx->a, &ctx->b, &ctx->c, &ctx->d, &ctx->scratch, &ctx->smmap, &ctx->pq, &ctx->pool_a, &ctx->pool_b, &ctx->need3, &ctx->spill})
     b->release();
   cudaStreamDestroy(ctx->stream);
+  cudaEventDestroy(ctx->done);
   delete ctx;
   return LC_OK;
 }
@@ -326,6 +342,10 @@ int walk_launch(lc_ctx* ctx, const WalkArgs& a, const uint64_t* d_starts, const 
   p.resume = resume;
   p.pool = pool;
   p.pool_count = pool_count;
+  // parked-lane capacity of the destination pool (the kernel never writes past it)
+  p.pool_cap = !pool ? 0
+               : (static_cast<void*>(pool) == ctx->pool_a.p ? ctx->pool_a.bytes : ctx->pool_b.bytes) /
+                     sizeof(lc::ResumeRec);
   p.park_below = pool ? park_below : 0u;
   p.n_dev = n_dev;
   p.park_min = park_min;
@@ -386,6 +406,7 @@ int lc_walk_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const ui
   a.hist_bins = hist_bins;
   LC_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  Ordered ord_(ctx, st);
   // Lane parking without a host sync (the call stays asynchronous): a fixed number of
   // resume rounds is queued, each reading its item count (the previous round's parked
   // lanes) on the device; a round with nothing parked exits at once, and the last round
@@ -432,6 +453,7 @@ int lc_walk(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const uint64_t*
   a.hist_shift = hist_shift;
   a.hist_bins = hist_bins;
   LC_CUDA(cudaSetDevice(ctx->device));
+  Ordered ord_(ctx, ctx->stream);
   const size_t sb = (LC_ST_HEADER + hist_bins + 2ull) * sizeof(uint64_t);
   const size_t nb = static_cast<size_t>(n) * sizeof(uint64_t);
   const size_t ob = nb * std::max<uint32_t>(legs, 1);
@@ -495,6 +517,7 @@ int lc_clock(lc_ctx* ctx, const lc_spec* spec, const uint64_t* xs, uint64_t n, u
   if (rc) return rc;
   if (n == 0) return LC_OK;
   LC_CUDA(cudaSetDevice(ctx->device));
+  Ordered ord_(ctx, ctx->stream);
   const size_t nb = static_cast<size_t>(n) * 8;
   LC_CUDA(ctx->a.ensure(nb));
   LC_CUDA(ctx->b.ensure(nb));
@@ -517,6 +540,7 @@ int lc_is_candidate(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const u
   if ((rc = check_fixed(id, fixed_r3))) return rc;
   if (n == 0) return LC_OK;
   LC_CUDA(cudaSetDevice(ctx->device));
+  Ordered ord_(ctx, ctx->stream);
   LC_CUDA(ctx->a.ensure(n * 8));
   LC_CUDA(ctx->b.ensure(n));
   LC_CUDA(cudaMemcpyAsync(ctx->a.p, xs, n * 8, cudaMemcpyHostToDevice, ctx->stream));
@@ -536,6 +560,7 @@ int lc_predecessors(lc_ctx* ctx, const lc_spec* spec, const uint64_t* xs, uint64
   if (rc) return rc;
   if (n == 0) return LC_OK;
   LC_CUDA(cudaSetDevice(ctx->device));
+  Ordered ord_(ctx, ctx->stream);
   LC_CUDA(ctx->a.ensure(n * 8));
   LC_CUDA(ctx->b.ensure(n * 32));
   LC_CUDA(ctx->c.ensure(n));
@@ -574,6 +599,7 @@ int lc_enumerate(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, uint64_t r
                  uint64_t* out, uint64_t cap, uint64_t* count) {
   if (!ctx || !count) return fail(LC_ERR_ARG, "null argument");
   LC_CUDA(cudaSetDevice(ctx->device));
+  Ordered ord_(ctx, ctx->stream);
   LC_CUDA(ctx->a.ensure(std::max<uint64_t>(cap, 1) * 8));
   LC_CUDA(ctx->d.ensure(8));
   int rc = lc_enumerate_device(ctx, spec, fixed_r3, r2_lo, r2_hi, ctx->a.as<uint64_t>(), cap,
@@ -608,6 +634,7 @@ int lc_random_candidates_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed
   if (n == 0) return LC_OK;
   LC_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  Ordered ord_(ctx, st);
   uint64_t trials = static_cast<uint64_t>(static_cast<double>(n) / acceptance_estimate(id)) + 65536;
   for (int attempt = 0; attempt < 8; ++attempt) {
     const uint64_t words = lc::random_scratch_words(trials);
@@ -635,6 +662,7 @@ int lc_random_candidates(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, ui
     return LC_OK;
   }
   LC_CUDA(cudaSetDevice(ctx->device));
+  Ordered ord_(ctx, ctx->stream);
   LC_CUDA(ctx->b.ensure(n * 8));
   int rc = lc_random_candidates_device(ctx, spec, fixed_r3, seed, n, ctx->b.as<uint64_t>(), ctx->stream);
   if (rc) return rc;
@@ -658,10 +686,9 @@ int lc_prune_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int32_t
   if (n == 0) return LC_OK;
   LC_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  Ordered ord_(ctx, st);
   LC_CUDA(ctx->pq.ensure(8));
   LC_CUDA(cudaMemsetAsync(ctx->pq.p, 0, 8, st));
-  const int ring = lc::prune_ring_for(n);
-  const int blocks = lc::prune_blocks_per_sm(id, ring) * ctx->sms;
 #ifndef LC_PRUNE_SPILL
 #define LC_PRUNE_SPILL 512
 #endif
@@ -669,10 +696,21 @@ int lc_prune_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int32_t
   // (testing: small values exercise the drop-and-climb fallback)
   uint32_t spill_cap = LC_PRUNE_SPILL;
   if (const char* env = getenv("LFSR_PRUNE_SPILL")) spill_cap = static_cast<uint32_t>(strtoul(env, nullptr, 10));
-  if (spill_cap) LC_CUDA(ctx->spill.ensure(lc::prune_spill_bytes(blocks, spill_cap)));
-  LC_CUDA(lc::launch_prune(id, static_cast<uint32_t>(fixed_r3), mode, limit, d_cands, n, d_removed, d_work,
-                           ctx->pq.as<unsigned long long>(), spill_cap ? ctx->spill.p : nullptr, spill_cap, ring, blocks,
-                           st));
+  const char* v1 = getenv("LFSR_PRUNE_V1");  // A/B: the round-1 kernel (64-bit node, no register cache)
+  if (v1 && v1[0] == '1') {
+    const int ring = lc::prune_ring_for(n);
+    const int blocks = lc::prune_blocks_per_sm(id, ring) * ctx->sms;
+    if (spill_cap) LC_CUDA(ctx->spill.ensure(lc::prune_spill_bytes(blocks, spill_cap)));
+    LC_CUDA(lc::launch_prune(id, static_cast<uint32_t>(fixed_r3), mode, limit, d_cands, n, d_removed, d_work,
+                             ctx->pq.as<unsigned long long>(), spill_cap ? ctx->spill.p : nullptr, spill_cap, ring,
+                             blocks, st));
+  } else {
+    const int blocks = lc::prune2_blocks_per_sm(id, mode) * ctx->sms;
+    if (spill_cap) LC_CUDA(ctx->spill.ensure(lc::prune2_spill_bytes(blocks, spill_cap)));
+    LC_CUDA(lc::launch_prune2(id, static_cast<uint32_t>(fixed_r3), mode, limit, d_cands, n, d_removed, d_work,
+                              ctx->pq.as<unsigned long long>(), spill_cap ? ctx->spill.p : nullptr, spill_cap, blocks,
+                              st));
+  }
   g_launches += 1;
   return LC_OK;
 }
@@ -682,6 +720,7 @@ int lc_prune(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int32_t mode, 
   if (!ctx) return fail(LC_ERR_ARG, "null context");
   if (n == 0) return LC_OK;
   LC_CUDA(cudaSetDevice(ctx->device));
+  Ordered ord_(ctx, ctx->stream);
   LC_CUDA(ctx->a.ensure(n * 8));
   LC_CUDA(ctx->b.ensure(n));
   LC_CUDA(ctx->c.ensure(n * 8));
@@ -703,6 +742,7 @@ int lc_first_missing(lc_ctx* ctx, const uint64_t* sorted_set, uint64_t m, const 
   *first_missing = n;
   if (n == 0) return LC_OK;
   LC_CUDA(cudaSetDevice(ctx->device));
+  Ordered ord_(ctx, ctx->stream);
   LC_CUDA(ctx->a.ensure(std::max<uint64_t>(m, 1) * 8));
   LC_CUDA(ctx->b.ensure(n * 8));
   LC_CUDA(ctx->d.ensure(8));
@@ -743,6 +783,7 @@ int lc_sort_edges(lc_ctx* ctx, uint64_t n, uint64_t* src, uint64_t* dst, uint64_
   if (n < 2) return LC_OK;
   if (!src || !dst || !dist) return fail(LC_ERR_ARG, "null buffer");
   LC_CUDA(cudaSetDevice(ctx->device));
+  Ordered ord_(ctx, ctx->stream);
   const size_t nb = n * 8;
   uint64_t* host[5] = {src, dst, dist, subtree_size, subtree_depth};
   DevBuf* bufs[5] = {&ctx->a, &ctx->b, &ctx->c, &ctx->d, &ctx->stats};
@@ -760,6 +801,24 @@ int lc_sort_edges(lc_ctx* ctx, uint64_t n, uint64_t* src, uint64_t* dst, uint64_
   for (int k = 0; k < 5; ++k)
     if (host[k]) LC_CUDA(cudaMemcpyAsync(host[k], dev[k], nb, cudaMemcpyDeviceToHost, ctx->stream));
   LC_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LC_OK;
+}
+
+int lc_sort_edges_device(lc_ctx* ctx, uint64_t n, const uint64_t* const* d_in, uint64_t* const* d_out,
+                         void* stream) {
+  if (!ctx || !d_in || !d_out) return fail(LC_ERR_ARG, "null argument");
+  if (n >= (1ull << 32)) return fail(LC_ERR_ARG, "at most 2^32 - 1 records per sort");
+  if (n == 0) return LC_OK;
+  if (!d_in[0] || !d_in[1] || !d_in[2] || !d_out[0] || !d_out[1] || !d_out[2]) return fail(LC_ERR_ARG, "null buffer");
+  for (int k = 0; k < 5; ++k)
+    if ((d_in[k] == nullptr) != (d_out[k] == nullptr)) return fail(LC_ERR_ARG, "column %d: input and output must both be set", k);
+  LC_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  Ordered ord_(ctx, st);
+  LC_CUDA(ctx->scratch.ensure(lc::radix_sort_scratch_bytes(n)));
+  int launches = 0;
+  LC_CUDA(lc::radix_sort_records(n, d_in, d_out, 5, ctx->scratch.p, ctx->scratch.bytes, st, &launches));
+  g_launches += launches;
   return LC_OK;
 }
 
@@ -785,6 +844,7 @@ int lc_cut_leaves(lc_ctx* ctx, uint64_t n, uint64_t* src, uint64_t* dst, uint64_
   if (n == 0) return empty_cut(pass_stats, max_stats, n_passes);
   if (!src || !dst || !dist || !subtree_size || !subtree_depth) return fail(LC_ERR_ARG, "null buffer");
   LC_CUDA(cudaSetDevice(ctx->device));
+  Ordered ord_(ctx, ctx->stream);
   const size_t nb = n * 8;
   DevBuf* cols[5] = {&ctx->a, &ctx->b, &ctx->c, &ctx->d, &ctx->stats};
   uint64_t* host[5] = {src, dst, dist, subtree_size, subtree_depth};
@@ -816,6 +876,7 @@ int lc_cut_leaves_device(lc_ctx* ctx, uint64_t n, uint64_t* src, uint64_t* dst, 
   if (n == 0) return empty_cut(pass_stats, max_stats, n_passes);
   if (!src || !dst || !dist || !subtree_size || !subtree_depth) return fail(LC_ERR_ARG, "null buffer");
   LC_CUDA(cudaSetDevice(ctx->device));
+  Ordered ord_(ctx, ctx->stream);
   // The passes are replayed from a CUDA graph, which cannot be captured on the legacy
   // default stream: wait for the caller's stream, then run on the context's own stream
   // (the call is synchronous, so the caller's later work sees the results).
@@ -944,6 +1005,7 @@ int lc_bf_build_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int 
   if (!d_succ || !d_indeg || !d_is_cand || !d_cycle_of) return fail(LC_ERR_ARG, "null buffer");
   LC_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  Ordered ord_(ctx, st);
   LC_CUDA(ctx->scratch.ensure(n * 8));
   int launches = 0;
   LC_CUDA(lc::bf_build(id, n, clock_all, static_cast<uint32_t>(fixed_r3), d_succ, d_indeg, d_is_cand, d_cycle_of,
@@ -973,6 +1035,7 @@ int lc_bf_segments_device(lc_ctx* ctx, uint64_t n, const int64_t* d_succ, const 
     return fail(LC_ERR_ARG, "null buffer");
   LC_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  Ordered ord_(ctx, st);
   const size_t bytes = lc::bf_segments_scratch(n);
   LC_CUDA(ctx->scratch.ensure(bytes));
   int launches = 0;
@@ -988,6 +1051,7 @@ int lc_bf_cycle_order_device(lc_ctx* ctx, uint64_t m, const int64_t* d_cs, int64
   if (m && (!d_cs || !d_start || !d_steps)) return fail(LC_ERR_ARG, "null buffer");
   LC_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  Ordered ord_(ctx, st);
   LC_CUDA(ctx->scratch.ensure(std::max<uint64_t>(m, 1) * 8 * 3));
   int64_t* t = ctx->scratch.as<int64_t>();
   int launches = 0;
@@ -1003,6 +1067,7 @@ int lc_count_cycles(lc_ctx* ctx, uint64_t n, const uint64_t* src, const uint64_t
   *n_cycles = 0;
   if (n == 0) return LC_OK;
   LC_CUDA(cudaSetDevice(ctx->device));
+  Ordered ord_(ctx, ctx->stream);
   const size_t nb = n * 8;
   DevBuf* in[4] = {&ctx->a, &ctx->b, &ctx->c, &ctx->d};
   const uint64_t* host[4] = {src, dst, dist, subtree_size};

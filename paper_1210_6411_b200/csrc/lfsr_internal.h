@@ -2,7 +2,29 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
+
+// Bounds / invariant checks of the checked build (-DLC_CHECKS=1, __graft_entry__.build()
+// writes it to _lib/checked/; tests/test_gpu_checked.py runs every kernel mode on it): a
+// failed check prints its site and traps, so the call fails with a CUDA error.  Compiled
+// out of the product library.
+#ifndef LC_CHECKS
+#define LC_CHECKS 0
+#endif
+#if LC_CHECKS
+#define LC_CHECK(c)                                                                \
+  do {                                                                             \
+    if (!(c)) {                                                                    \
+      printf("LC_CHECK failed at %s:%d: %s\n", __FILE__, __LINE__, #c);            \
+      __trap();                                                                    \
+    }                                                                              \
+  } while (0)
+#else
+#define LC_CHECK(c) \
+  do {              \
+  } while (0)
+#endif
 
 #include "../../include/lfsr_b200.h"
 
@@ -20,7 +42,7 @@ struct LaneMeta {
   uint64_t arm_at;     // warp clock from which the lane may report a special node
   uint64_t deadline;   // warp clock of the cap audit
   uint32_t legs_done;
-  uint32_t pad;
+  uint32_t pad;        // 1: the cap audit excused this leg once (inside a fixed-R3 run)
 };
 
 // A parked lane (lane mode): state and leg bookkeeping relative to the parking clock, so
@@ -32,7 +54,7 @@ struct ResumeRec {
   uint64_t arm_rel;   // clocks until the lane may report (0: armed)
   uint64_t dead_rel;  // clocks until the cap audit (kInf: none)
   uint32_t legs_done;
-  uint32_t pad;
+  uint32_t pad;       // LaneMeta::pad
 };
 
 struct WalkParams {
@@ -67,6 +89,7 @@ struct WalkParams {
   uint32_t pad3;
   const unsigned long long* n_dev;  // resume round queued without a host sync: item count on the device (else null)
   uint64_t park_min;                // park only while the round has more than this many items
+  uint64_t pool_cap;                // ResumeRec slots in `pool` (a warp that does not fit keeps walking)
 };
 
 // Launchers (defined in the .cu files); all enqueue on `stream`.
@@ -112,6 +135,14 @@ cudaError_t launch_prune(SpecId id, uint32_t F, int mode, uint64_t limit, const 
 // ring below 2^24 (tail-bound), the wide-occupancy one above (LFSR_PRUNE_RING forces 20/32).
 int prune_ring_for(uint64_t n);
 int prune_blocks_per_sm(SpecId id, int ring);
+
+// K3 v2 (csrc/prune.cu): 32-bit node registers, register-cached pending entries; same
+// results as launch_prune.  mode 0 = dfs, 1 = bfs.
+int prune2_blocks_per_sm(SpecId id, int mode);
+uint64_t prune2_spill_bytes(int blocks, uint32_t cap);
+cudaError_t launch_prune2(SpecId id, uint32_t F, int mode, uint64_t limit, const uint64_t* cands, uint64_t n,
+                          uint8_t* removed, uint64_t* work, unsigned long long* queue, void* spill,
+                          uint32_t spill_cap, int blocks, cudaStream_t stream);
 
 cudaError_t measure_lop3_peak(int sms, double* ops_per_s, double* sm_mhz);
 
@@ -184,6 +215,10 @@ cudaError_t pack_records_device(uint64_t n, const uint64_t* src, const uint64_t*
                                 const uint64_t* size, const uint64_t* depth, uint64_t* out, cudaStream_t st,
                                 int* launches);
 size_t sort_scratch_bytes(uint64_t n);
+// In-house LSD radix sort (csrc/sort.cu): cols_in[0] = keys; out of place; n < 2^32.
+size_t radix_sort_scratch_bytes(uint64_t n);
+cudaError_t radix_sort_records(uint64_t n, const uint64_t* const* cols_in, uint64_t* const* cols_out, int ncols,
+                               void* scratch, size_t scratch_bytes, cudaStream_t st, int* launches);
 cudaError_t sort_records_device(uint64_t n, uint64_t* const* cols, int ncols, void* scratch, size_t scratch_bytes,
                                 cudaStream_t st, int* launches);
 

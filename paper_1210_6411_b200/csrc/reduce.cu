@@ -11,7 +11,6 @@
 // the reference's fixpoint and per-pass statistics exactly, without external sorts.
 // Cycles: pointer jumping labels every record with the smallest index on its cycle (the
 // smallest source, since sources ascend), then one atomic fold per record.
-#include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -400,15 +399,6 @@ __global__ void select_kernel(const uint64_t* __restrict__ newpos, uint64_t n, c
   }
 }
 
-__global__ void gather_kernel(const uint64_t* __restrict__ order, uint64_t n, const uint64_t* __restrict__ a,
-                              uint64_t* __restrict__ b) {
-  GRID_STRIDE(i, n) { b[i] = a[order[i]]; }
-}
-
-__global__ void iota_kernel(uint64_t* v, uint64_t n) {
-  GRID_STRIDE(i, n) { v[i] = i; }
-}
-
 }  // namespace
 
 // Scratch layout helper: allocate on demand from one buffer.
@@ -789,39 +779,25 @@ cudaError_t pack_records_device(uint64_t n, const uint64_t* src, const uint64_t*
 
 // Edge-output stage: records sorted ascending by source, the
 // precondition of the edge file format and of step 4 (records.py:3-5, reduce.py:3-4).
-// LSD radix sort of (source, row) pairs (CUB), then a gather of the other columns.
-size_t sort_scratch_bytes(uint64_t n) {
-  size_t temp = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, temp, static_cast<const uint64_t*>(nullptr), static_cast<uint64_t*>(nullptr),
-                                  static_cast<const uint64_t*>(nullptr), static_cast<uint64_t*>(nullptr),
-                                  static_cast<int64_t>(n));
-  return temp + 4 * n * 8 + 4 * 256;
-}
+// The in-house radix sort (csrc/sort.cu) writes out of place into scratch; the sorted
+// columns are copied back.
+size_t sort_scratch_bytes(uint64_t n) { return radix_sort_scratch_bytes(n) + 5 * ((n * 8 + 255) & ~255ull); }
 
 // cols[0] is the key column; cols[1..ncols) (non-null) are permuted alongside it.
 cudaError_t sort_records_device(uint64_t n, uint64_t* const* cols, int ncols, void* scratch, size_t scratch_bytes,
                                 cudaStream_t st, int* launches) {
   if (n < 2) return cudaSuccess;
-  ReduceScratch s{static_cast<uint8_t*>(scratch), 0};
-  uint64_t* order_in = s.take<uint64_t>(n);
-  uint64_t* order = s.take<uint64_t>(n);
-  uint64_t* keys = s.take<uint64_t>(n);
-  uint64_t* tmp = s.take<uint64_t>(n);
-  void* temp = static_cast<uint8_t*>(scratch) + s.used;
-  size_t temp_bytes = scratch_bytes - s.used;
-  iota_kernel<<<grid_for(n), kT, 0, st>>>(order_in, n);
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, cols[0], keys, order_in, order,
-                                                  static_cast<int64_t>(n), 0, 64, st);
+  const size_t col_bytes = (n * 8 + 255) & ~255ull;
+  uint8_t* p = static_cast<uint8_t*>(scratch);
+  uint64_t* out[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  for (int k = 0; k < ncols; ++k) out[k] = cols[k] ? reinterpret_cast<uint64_t*>(p + k * col_bytes) : nullptr;
+  const size_t used = 5 * col_bytes;
+  cudaError_t e = radix_sort_records(n, cols, out, ncols, p + used, scratch_bytes - used, st, launches);
   if (e != cudaSuccess) return e;
-  *launches += 2;  // iota + the radix sort (several CUB kernels)
-  for (int k = 1; k < ncols; ++k) {
-    if (!cols[k]) continue;
-    gather_kernel<<<grid_for(n), kT, 0, st>>>(order, n, cols[k], tmp);
-    if ((e = cudaMemcpyAsync(cols[k], tmp, n * 8, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
-    ++*launches;
-  }
-  if ((e = cudaMemcpyAsync(cols[0], keys, n * 8, cudaMemcpyDeviceToDevice, st)) != cudaSuccess) return e;
-  return cudaGetLastError();
+  for (int k = 0; k < ncols; ++k)
+    if (cols[k] && (e = cudaMemcpyAsync(cols[k], out[k], n * 8, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+      return e;
+  return cudaSuccess;
 }
 
 }  // namespace lc

@@ -213,6 +213,7 @@ __device__ __forceinline__ void whole_warp_refill(const WalkParams& p, volatile 
         m.deadline = 0;  // (identical for every lane of the item)
         m.legs_done = 0u;
         m.pad = 0u;
+        LC_CHECK(k < p.n);
         p.meta[(wbase + r) * 32u + lane] = m;
       }
     }
@@ -283,6 +284,7 @@ __device__ __forceinline__ void lane_refill(const WalkParams& p, volatile WalkSh
       const uint64_t k = (b + j_item) * p.nq + qi;
       if (p.resume) {
         // a parked lane: same leg, clocks re-based on this warp's clock (mod 2^64)
+        LC_CHECK(k < sh.n);
         const ResumeRec rec = p.resume[k];
         insert_lane<S::NB>(s, j, rec.state);
         LaneMeta m;
@@ -291,13 +293,14 @@ __device__ __forceinline__ void lane_refill(const WalkParams& p, volatile WalkSh
         m.arm_at = sat_add(t, rec.arm_rel);
         m.deadline = rec.dead_rel == kInf ? kInf : sat_add(t, rec.dead_rel);
         m.legs_done = rec.legs_done;
-        m.pad = 0u;
+        m.pad = rec.pad;
         meta[j] = m;
         active |= 1u << j;
         next_arm = min(next_arm, m.arm_at);
         next_dead = min(next_dead, m.deadline);
         continue;
       }
+      LC_CHECK(k < p.n);
       const uint64_t x = p.starts[k] & kStateMask;
       const uint32_t r1 = static_cast<uint32_t>(x & S::M1);
       const uint32_t r2 = static_cast<uint32_t>((x >> S::O2) & S::M2);
@@ -333,7 +336,7 @@ __device__ __forceinline__ void lane_refill(const WalkParams& p, volatile WalkSh
 // retires; the host relaunches on the pool with the lanes packed densely, so warps stay
 // full through the tail of wide-spread walks (random starts, several hops).
 template <class S>
-__device__ __forceinline__ void park_lanes(const WalkParams& p, volatile WalkShared& sh, const uint32_t (&s)[S::NB]) {
+__device__ __forceinline__ bool park_lanes(const WalkParams& p, volatile WalkShared& sh, const uint32_t (&s)[S::NB]) {
   const uint32_t tid = tid_x(), lane = tid & 31u, w = tid >> 5;
   const uint64_t gtid = static_cast<uint64_t>(ctaid_x()) * kWalkThreads + tid;
   const LaneMeta* const meta = p.meta + gtid * 32u;
@@ -346,8 +349,23 @@ __device__ __forceinline__ void park_lanes(const WalkParams& p, volatile WalkSha
     const uint32_t v = __shfl_up_sync(kFull, incl, o);
     if (lane >= static_cast<uint32_t>(o)) incl += v;
   }
+  // reserve the warp's slots only if they fit in the pool (else the warp keeps walking)
   unsigned long long base = 0;
-  if (lane == 31u) base = atomicAdd(p.pool_count, static_cast<unsigned long long>(incl));
+  uint32_t fits = 1u;
+  if (lane == 31u) {
+    unsigned long long old = atomicAdd(p.pool_count, 0ull);
+    for (;;) {
+      if (old + incl > p.pool_cap) {
+        fits = 0u;
+        break;
+      }
+      const unsigned long long prev = atomicCAS(p.pool_count, old, old + incl);
+      if (prev == old) break;
+      old = prev;
+    }
+    base = old;
+  }
+  if (!__shfl_sync(kFull, fits, 31)) return false;
   base = __shfl_sync(kFull, base, 31) + (incl - cnt);
   for (uint32_t a = act; a != 0u; a &= a - 1u, ++base) {
     const int j = __ffs(a) - 1;
@@ -359,11 +377,13 @@ __device__ __forceinline__ void park_lanes(const WalkParams& p, volatile WalkSha
     r.arm_rel = ((armed >> j) & 1u) || m.arm_at <= t ? 0ull : m.arm_at - t;
     r.dead_rel = m.deadline == kInf ? kInf : (m.deadline > t ? m.deadline - t : 0ull);
     r.legs_done = m.legs_done;
-    r.pad = 0u;
+    r.pad = m.pad;  // cap deadline already excused once
+    LC_CHECK(base < p.pool_cap);
     p.pool[base] = r;
   }
   sh.active[tid] = 0u;
   __syncwarp();
+  return true;
 }
 
 // Arm (check every step) once R3 is this close to F.  Whole-warp mode: lanes of a warp
@@ -371,7 +391,8 @@ __device__ __forceinline__ void park_lanes(const WalkParams& p, volatile WalkSha
 // while it skips a long stretch (stride-1 walks: 2.8e6 checked steps per walk otherwise);
 // lane mode: lanes are independent, so a tight bound pays.
 constexpr uint64_t kArmSlackWarp = 1u << 16, kArmSlackLane = 1u << 10;
-constexpr uint64_t kArmBatch = 1u << 12;  // re-arm lanes due this soon in the same event
+constexpr uint64_t kArmBatch = 1u << 12;
+constexpr uint64_t kRunSlack = 128;  // clocks granted to finish a fixed-R3 run at the cap audit  // re-arm lanes due this soon in the same event
 
 // R3 of lane j (bits o3 .. o3 + l3 - 1 of its state).
 template <class S>
@@ -415,6 +436,7 @@ __device__ __forceinline__ void handle_events(const WalkParams& p, volatile Walk
         m.leg_start = t;
         m.arm_at = sat_add(t, S::WINDOW);
         m.deadline = sat_add(t, p.cap1);
+        m.pad = 0u;
       }
       meta[j] = m;
     }
@@ -457,8 +479,19 @@ __device__ __forceinline__ void handle_events(const WalkParams& p, volatile Walk
       const int j = __ffs(a) - 1;
       const uint64_t dl = meta[j].deadline;
       if (dl <= t) {
-        if (!((on_plane >> j) & 1u)) raise_error(p.stats, LC_ERR_CAP, meta[j].walk);
-        meta[j].deadline = kInf;
+        // Excused once: the run of fixed-R3 states ends within kRunSlack clocks (R3
+        // stays put only while R1 and R2 both clock with clock bits equal to each other,
+        // and a maximal-period register repeats a bit at most L times in a row), and its
+        // last state is the special node (its predecessor is the previous state).  A lane
+        // still searching at the excused deadline raises like any other.
+        if (!((on_plane >> j) & 1u) || meta[j].pad) {
+          raise_error(p.stats, LC_ERR_CAP, meta[j].walk);
+          meta[j].deadline = kInf;
+        } else {
+          meta[j].pad = 1u;
+          meta[j].deadline = t + kRunSlack;
+          next_dead = min(next_dead, t + kRunSlack);
+        }
       } else {
         next_dead = min(next_dead, dl);
       }
@@ -533,8 +566,7 @@ __global__ void __launch_bounds__(kWalkThreads, LC_WALK_MIN_BLOCKS) walk_kernel(
       }
       if (sh.park && !sh.open[w] &&
           __reduce_add_sync(kFull, static_cast<uint32_t>(__popc(sh.active[tid]))) < p.park_below) {
-        park_lanes<S>(p, sh, s);
-        break;
+        if (park_lanes<S>(p, sh, s)) break;
       }
       // ---- next warp-wide event horizon
       const uint64_t t = sh.t[w];

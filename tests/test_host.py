@@ -314,6 +314,15 @@ def test_package_exports_reference_namespace():
              "ExpectationTable SampleStats deviation_report random_mapping_expectations "
              "sample_segment_distances sample_segment_shapes").split()
     assert [n for n in names if not hasattr(pkg, n)] == []
+    # the reference's submodules exist under the same names (lfsrcycles.<module>)
+    import importlib
+
+    for mod, attrs in {"cipher": ("A51", "predecessors"), "bitslice": ("forward_to_candidate",),
+                       "pipeline": ("prune_shallow_segments", "random_candidate"), "records": ("write_edges",),
+                       "reduce": ("cut_leaves_to_fixpoint",), "oracle": ("brute_force_analysis", "GroundTruth"),
+                       "stats": ("sample_segment_distances",)}.items():
+        m = importlib.import_module(f"paper_1210_6411_b200.{mod}")
+        assert all(hasattr(m, a) for a in attrs), mod
 
 
 def test_missing_library_fails_loudly(tmp_path):

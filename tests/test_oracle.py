@@ -150,3 +150,54 @@ def test_reduce_restatement_matches_reference(specs):
         one = reduce_np.cut_leaves(g["src"], g["dst"], g["dist"], z, z, max_passes=1)
         assert list(one[5][0]) == [want["pass1"][k] for k in ("leaves_removed", "inner_nodes", "out_size_sum")]
         assert u64_digest(np.stack(one[:5], 1).reshape(-1)) == want["pass1"]["records_digest"]
+
+
+def _avx512():
+    try:
+        return "avx512f" in open("/proc/cpuinfo").read()
+    except OSError:
+        return False
+
+
+@pytest.mark.skipif(not _avx512(), reason="oracle/walk512.c needs AVX-512 (build container only)")
+def test_walk512_pinned_on_the_reference_config1_run():
+    """oracle/walk512.c (the generator of the config-2 digests) reproduces the reference's
+    own config-1 run (65,536 walks, _edges_chunk over a process pool) and the 256-walk KAT
+    before its 2^24-walk output is trusted (tests/golden/a51_c2_digests.json)."""
+    import ctypes as C
+    import hashlib
+    import os
+    import subprocess
+
+    from conftest import ROOT
+
+    odir = os.path.join(ROOT, "oracle")
+    subprocess.run(["make", "-s", "-C", odir, "walk512"], check=True)
+    lib = C.CDLL(os.path.join(odir, "_build", "libwalk512.so"))
+    u = C.POINTER(C.c_uint64)
+    lib.w512_walk.argtypes = [C.c_uint32, u, C.c_uint64, C.c_uint64, C.c_uint64, u, u, u]
+
+    def walk(starts):
+        starts = np.ascontiguousarray(starts, dtype=np.uint64)
+        dst, dist, bad = (np.zeros(starts.size, np.uint64) for _ in range(3))
+        p = lambda a: a.ctypes.data_as(u)  # noqa: E731
+        assert lib.w512_walk(0x2AAA00, p(starts), starts.size, 11_170_000, 178_957_008, p(dst), p(dist), p(bad)) == 0
+        return dst, dist
+
+    kat = golden_npz("a51_kat256")
+    d, w = walk(kat["src"])
+    assert (d == kat["dst"]).all() and (w == kat["dist"]).all()
+    c1 = golden_json("a51_c1_65536.json")
+    c2 = golden_json("a51_c2_digests.json")
+    sample = golden_npz("a51_c1_sample")
+    from paper_1210_6411_b200 import A51, CandidateParams
+    from paper_1210_6411_b200.pipeline import reference_candidates
+
+    starts = reference_candidates(A51, CandidateParams.from_spec(A51, 0x2AAA00), 0, 1 << 16)
+    assert (starts[sample["idx"].astype(np.int64)] == sample["src"]).all()
+    d, w = walk(starts)
+    assert hashlib.sha256(d.astype("<u8").tobytes()).hexdigest() == c1["dst_digest"]
+    assert hashlib.sha256(w.astype("<u8").tobytes()).hexdigest() == c1["dist_digest"]
+    # the committed config-2 batches: batch 0's first 2^16 rows are config 1
+    assert c2["c1_prefix_starts_digest"] == c1["starts_digest"] and c2["n"] == 1 << 24
+    assert sum(b["sum_dist"] for b in c2["batches"]) == c2["sum_dist"]
