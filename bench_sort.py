@@ -5,10 +5,11 @@ resident, out of place.
     python bench_sort.py [--log2 24,26,28] [--keys a51|random64] [--reps 3]
 
 Prints one JSON line per size: time per sort, records/s, and the HBM roofline of the
-whole sort and of its pass kernel.  Algorithmic bytes per record: histogram 8 (key read);
-each pass that runs 24 (key + row in, key + row out; the first pass has no row to read:
-20); the gather 4 (row) + 8 (key) + 4 x 8 payload reads + 5 x 8 writes = 84.  L2 is
-flushed before every timed sort.  Parity: the output equals numpy's stable argsort order
+whole sort.  Algorithmic bytes per record: histogram + payload pack 72 (key and four
+payload columns read, the 32-byte record-major payload written); the first pass 20 (key
+in; key + row out); each middle pass 24 (key + row in and out); the last pass 84 (key +
+row in, the record's 32-byte payload, five output columns).  L2 is flushed before every
+timed sort.  Parity: the output equals numpy's stable argsort order
 (checked at the smallest size).
 """
 
@@ -83,7 +84,7 @@ def main():
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
         s = min(times)
-        alg = n * (8 + 20 + 24 * (varying_bytes - 1) + 84)
+        alg = n * (72 + 20 + 24 * (varying_bytes - 2) + 84)
         line = {"metric": "edge-output sort (5-column records by source)", "records": n, "keys": args.keys,
                 "passes_run": varying_bytes, "seconds": s, "records_per_s": n / s,
                 "roofline": {"bound": "hbm", "achieved": alg / s / 1e9, "peak": hbm / 1e9 if hbm else None,

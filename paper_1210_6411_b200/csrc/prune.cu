@@ -370,7 +370,7 @@ __device__ __forceinline__ int prune_step_unified(const uint8_t* tbl, uint32_t& 
 }
 
 #ifndef LC_PRUNE2_UNIFIED
-#define LC_PRUNE2_UNIFIED 0
+#define LC_PRUNE2_UNIFIED 1  // 0: the two-path step (A/B)
 #endif
 template <class S, int R, bool DFS>
 __device__ __forceinline__ int prune_step2(const uint8_t* tbl, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t& d,

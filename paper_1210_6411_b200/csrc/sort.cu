@@ -1,24 +1,28 @@
 // Edge-output sort: records ascending by source, the invariant
 // of the edge file and of step 4 (records.py:3-5, reduce.py:3-4).
 //
-// An LSD radix sort of the 64-bit source keys with a 32-bit row index as payload, one
-// byte per pass, each pass a single "onesweep" kernel (no separate upsweep per pass):
-//   * one histogram kernel reads the keys once and counts all eight byte digits (warp
-//     match-aggregated shared atomics), and notes whether the keys are already ascending;
-//   * a one-block scan turns the counts into per-byte digit starts and marks trivial
+// An LSD radix sort of the 64-bit source keys, one byte per pass, each pass a single
+// "onesweep" kernel (no separate upsweep per pass):
+//   * one histogram kernel reads the keys once and counts all eight byte digits
+//     (block-shared counters; a digit shared by the whole warp -- a constant byte -- is
+//     one add), and notes whether the keys are already ascending;
+//   * a one-block plan kernel turns the counts into per-byte digit starts, marks trivial
 //     bytes (every key in one bucket -- for A5/1 skeletons the R3 bytes, which all equal
-//     the fixed value -- or an already sorted input): their pass kernels return at once,
-//     and the ping-pong buffer of every pass is decided on the device, so the whole sort is
-//     enqueued without a host round trip;
-//   * a pass kernel takes tiles of 4096 keys in launch order (an atomic ticket, so a
-//     tile's predecessors are always resident), ranks each key within its warp (match on
-//     the digit, warp-private counters), scans the tile's 256 digit counts, publishes them
-//     and looks back over earlier tiles for each digit's global offset (decoupled
-//     look-back: 256 independent chains, one per thread), stages the tile in shared memory
-//     in digit order and writes each digit's run contiguously.  Ranking in input order
-//     makes every pass stable, so equal sources keep their input order (numpy's stable
-//     argsort).
-// The other record columns are then gathered by the final row index.
+//     the fixed value -- or an already sorted input; their pass kernels return at once)
+//     and assigns the ping-pong buffers backwards from the last pass that runs, so the
+//     whole sort is enqueued without a host round trip;
+//   * a pass kernel takes tiles of 3072 keys in launch order (an atomic ticket, so a
+//     tile's predecessors are always resident): it loads the tile's keys into registers
+//     and its row payload into shared memory (cp.async, overlapping the ranking), ranks
+//     each key within its warp (match on the digit, warp-private counters), publishes
+//     the tile's 256 digit counts and looks back over earlier tiles for each digit's
+//     global offset (decoupled look-back: 256 independent chains, one per thread), stages
+//     the tile in shared memory in digit order and writes each digit's run contiguously.
+//     Ranking in input order makes every pass stable, so equal sources keep their input
+//     order (numpy's stable argsort).
+//   * The last pass that runs writes the output key column and gathers the payload
+//     columns (destination, distance, subtree size/depth) by row directly into the
+//     output columns -- no separate gather pass.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -29,26 +33,41 @@
 namespace lc {
 namespace {
 
+#ifndef LC_SORT_MATCH_ANY
+#define LC_SORT_MATCH_ANY 0  // 1: rank with __match_any_sync (A/B)
+#endif
+
 constexpr uint32_t kFullMask = 0xffffffffu;
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kItems = 16;                          // keys per thread
-constexpr int kTileKeys = kSortThreads * kItems;    // 4096
+constexpr int kItems = 12;                          // keys per thread
+constexpr int kTileKeys = kSortThreads * kItems;    // 3072
 constexpr int kBins = 256;
 constexpr int kBytes = 8;
+constexpr int kCols = 5;
 // look-back status word: [49:48] flag, [47:40] epoch (pass byte + 1), [39:0] count
 constexpr uint64_t kFlagAgg = 1ull << 48, kFlagPrefix = 2ull << 48;
 constexpr uint64_t kValueMask = (1ull << 40) - 1;
 
 struct SortCtl {
-  unsigned long long hist[kBytes][kBins];  // digit counts, then (scan) digit starts
+  unsigned long long hist[kBytes][kBins];  // digit counts, then (plan) digit starts
   unsigned int tickets[kBytes];
   unsigned int unsorted;
   unsigned int trivial[kBytes];
-  unsigned int in_buf[kBytes];  // ping-pong buffer each pass reads
-  unsigned int first[kBytes];   // 1: the first pass that runs (payload = row index)
-  unsigned int final_buf;       // buffer holding the result (0: the input, never permuted)
+  unsigned int in_buf[kBytes];  // buffer a pass reads (keys / rows), 2 = the input column
+  unsigned int last[kBytes];    // 1: the last pass that runs (writes the output columns)
   unsigned int passes;
+};
+
+struct Cols {
+  const uint64_t* in[kCols];
+  uint64_t* out[kCols];
+};
+
+// keys[0] = output key column, keys[1] = scratch; rows[0..1] scratch
+struct PassBufs {
+  uint64_t* keys[2];
+  uint32_t* rows[2];
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -57,8 +76,33 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+// Lanes holding the same 9-bit digit (256 = past the end): one ballot per bit
+// (MATCH.ANY serialises over the distinct values of a warp, 32 for random digits).
+__device__ __forceinline__ uint32_t peers_of(uint32_t d) {
+#if LC_SORT_MATCH_ANY
+  return __match_any_sync(kFullMask, d);
+#else
+  uint32_t m = kFullMask;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    const uint32_t b = __ballot_sync(kFullMask, (d >> i) & 1u);
+    m &= ((d >> i) & 1u) ? b : ~b;
+  }
+  return m;
+#endif
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Also packs the payload columns record-major (32 B per record: destination, distance,
+// subtree size, subtree depth; missing columns as 0), so the last pass fetches one
+// aligned 32-byte sector per record instead of one scattered sector per column.
 __global__ void __launch_bounds__(kSortThreads) sort_hist_kernel(const uint64_t* __restrict__ keys, uint64_t n,
-                                                                 SortCtl* ctl) {
+                                                                 SortCtl* ctl, Cols cols, ulonglong2* __restrict__ aos) {
   __shared__ unsigned int h[kBytes][kBins];
   for (int i = threadIdx.x; i < kBytes * kBins; i += kSortThreads) (&h[0][0])[i] = 0;
   __syncthreads();
@@ -69,12 +113,21 @@ __global__ void __launch_bounds__(kSortThreads) sort_hist_kernel(const uint64_t*
     const bool ok = i < n;
     const uint64_t k = ok ? keys[i] : 0;
     if (ok && i + 1 < n) descent |= k > keys[i + 1];
+    if (ok) {
+      aos[2 * i] = make_ulonglong2(cols.in[1] ? cols.in[1][i] : 0ull, cols.in[2] ? cols.in[2][i] : 0ull);
+      aos[2 * i + 1] = make_ulonglong2(cols.in[3] ? cols.in[3][i] : 0ull, cols.in[4] ? cols.in[4][i] : 0ull);
+    }
     const uint32_t live = __ballot_sync(kFullMask, ok);
 #pragma unroll
     for (int b = 0; b < kBytes; ++b) {
-      const uint32_t d = ok ? static_cast<uint32_t>(k >> (8 * b)) & 0xffu : 0x100u;
-      const uint32_t peers = __match_any_sync(kFullMask, d) & live;
-      if (ok && (peers & lanemask_lt()) == 0u) atomicAdd(&h[b][d], __popc(peers));
+      const uint32_t d = static_cast<uint32_t>(k >> (8 * b)) & 0xffu;
+      const uint32_t d0 = __shfl_sync(kFullMask, d, 0);  // every lane takes part (no short circuit)
+      const bool uniform = __all_sync(kFullMask, !ok || d == d0);
+      if (uniform) {
+        if ((threadIdx.x & 31) == 0) atomicAdd(&h[b][d], __popc(live));
+      } else if (ok) {
+        atomicAdd(&h[b][d], 1u);
+      }
     }
   }
   if (__syncthreads_or(descent) && threadIdx.x == 0) atomicOr(&ctl->unsorted, 1u);
@@ -84,7 +137,9 @@ __global__ void __launch_bounds__(kSortThreads) sort_hist_kernel(const uint64_t*
   }
 }
 
-// One block: digit starts per byte, trivial bytes, the buffer each pass reads.
+// One block: digit starts per byte, trivial bytes, and the buffers: the last pass that
+// runs writes the output columns, so buffers alternate backwards from it; the first reads
+// the input key column and makes up the row payload.
 __global__ void __launch_bounds__(kBins) sort_plan_kernel(uint64_t n, SortCtl* ctl) {
   __shared__ unsigned long long part[kBins];
   __shared__ unsigned int triv;
@@ -107,71 +162,77 @@ __global__ void __launch_bounds__(kBins) sort_plan_kernel(uint64_t n, SortCtl* c
     __syncthreads();
   }
   if (d == 0) {
-    unsigned int buf = 0, runs = 0;
+    unsigned int runs = 0;
+    for (int b = 0; b < kBytes; ++b) runs += ctl->trivial[b] ? 0u : 1u;
+    unsigned int j = 0;  // index among the passes that run
     for (int b = 0; b < kBytes; ++b) {
-      ctl->in_buf[b] = buf;
-      ctl->first[b] = runs == 0u;
-      if (!ctl->trivial[b]) {
-        buf ^= 1u;
-        ++runs;
-      }
+      ctl->last[b] = 0u;
+      ctl->in_buf[b] = 0u;
+      if (ctl->trivial[b]) continue;
+      // pass j writes buffer (runs - 1 - j) & 1 (the last one: 0 = the output key column),
+      // so it reads what pass j - 1 wrote, (runs - j) & 1; pass 0 reads the input (2)
+      ctl->in_buf[b] = j == 0 ? 2u : ((runs - j) & 1u);
+      ctl->last[b] = j + 1 == runs;
+      ++j;
     }
-    ctl->final_buf = buf;
     ctl->passes = runs;
   }
 }
 
-// Ping-pong buffers: keys[0] is the output key column, keys[1] scratch; the first pass
-// that runs reads the (read-only) input key column instead and generates the row index.
-struct PassBufs {
-  const uint64_t* kfirst;
-  uint64_t* keys[2];
-  uint32_t* rows[2];
-};
+constexpr int kWhistStride = kBins + 1;  // one spare counter per warp for lanes past the end
+constexpr size_t kSmemKeys = kTileKeys * 8, kSmemRows = kTileKeys * 4;
+constexpr size_t kPassSmem = kSmemKeys + 2 * kSmemRows + (kSortWarps * kWhistStride + 8) * 4 + kBins * 8 + kBins * 4;
 
-struct Cols {
-  const uint64_t* in[5];
-  uint64_t* out[5];
-};
-
-__global__ void __launch_bounds__(kSortThreads) sort_pass_kernel(PassBufs bufs, uint64_t n, int byte, SortCtl* ctl,
-                                                                 uint64_t* status) {
+__global__ void __launch_bounds__(kSortThreads, 3) sort_pass_kernel(PassBufs bufs, Cols cols, uint64_t n, int byte,
+                                                                    SortCtl* ctl, uint64_t* status,
+                                                                    const ulonglong2* __restrict__ aos) {
   if (ctl->trivial[byte]) return;
   extern __shared__ __align__(16) uint8_t smem[];
-  uint64_t* skeys = reinterpret_cast<uint64_t*>(smem);                              // [kTileKeys]
-  uint32_t* srows = reinterpret_cast<uint32_t*>(skeys + kTileKeys);                 // [kTileKeys]
-  uint32_t* whist = srows + kTileKeys;                                              // [kSortWarps][kBins + 1]
-  unsigned long long* gbase = reinterpret_cast<unsigned long long*>(whist + kSortWarps * (kBins + 1));  // [kBins] (8-aligned: 8 * 257 words)
-  uint32_t* loff = reinterpret_cast<uint32_t*>(gbase + kBins);                      // [kBins]
+  uint64_t* skeys = reinterpret_cast<uint64_t*>(smem);                         // staged keys [kTileKeys]
+  uint32_t* srows = reinterpret_cast<uint32_t*>(smem + kSmemKeys);             // staged rows [kTileKeys]
+  uint32_t* irows = reinterpret_cast<uint32_t*>(smem + kSmemKeys + kSmemRows); // input rows, input order
+  uint32_t* whist = irows + kTileKeys;                                         // [kSortWarps][kWhistStride]
+  unsigned long long* gbase = reinterpret_cast<unsigned long long*>(whist + kSortWarps * kWhistStride + 8);
+  uint32_t* loff = reinterpret_cast<uint32_t*>(gbase + kBins);
   __shared__ unsigned int tile_s;
+  __shared__ uint32_t wsum[kSortWarps];
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) tile_s = atomicAdd(&ctl->tickets[byte], 1u);
-  for (int i = tid; i < kSortWarps * (kBins + 1); i += kSortThreads) whist[i] = 0;
+  for (int i = tid; i < kSortWarps * kWhistStride; i += kSortThreads) whist[i] = 0;
   __syncthreads();
   const uint64_t tile = tile_s;
   const uint64_t t0 = tile * kTileKeys;
+  const uint32_t tn = static_cast<uint32_t>(n - t0 < static_cast<uint64_t>(kTileKeys) ? n - t0 : kTileKeys);
   const uint32_t ib = ctl->in_buf[byte];
-  const bool first = ctl->first[byte] != 0u;
-  const uint64_t* __restrict__ kin = first ? bufs.kfirst : bufs.keys[ib];
-  const uint32_t* __restrict__ rin = bufs.rows[ib];
+  const bool first = ib == 2u, last = ctl->last[byte] != 0u;
+  const uint64_t* __restrict__ kin = first ? cols.in[0] : bufs.keys[ib];
   const int shift = 8 * byte;
 
-  // ---- load (warp-striped: item k of lane l is key w*512 + k*32 + l) and rank per warp
+  // ---- the row payload to shared memory in input order (async), keys to registers
+  if (!first) {
+    const uint32_t* __restrict__ rin = bufs.rows[ib] + t0;
+    if (tn == static_cast<uint32_t>(kTileKeys)) {
+      for (int c = tid; c < kTileKeys / 4; c += kSortThreads) cp_async16(irows + 4 * c, rin + 4 * c);
+    } else {
+      for (uint32_t j = tid; j < tn; j += kSortThreads) irows[j] = rin[j];
+    }
+  }
   uint64_t key[kItems];
   uint32_t rank[kItems];
-  uint32_t* wh = whist + w * (kBins + 1);
+#pragma unroll
+  for (int k = 0; k < kItems; ++k) {
+    const uint32_t j = static_cast<uint32_t>(w * (32 * kItems) + k * 32 + lane);
+    key[k] = j < tn ? kin[t0 + j] : ~0ull;
+  }
+  // ---- rank within the warp (warp-striped: item k of lane l is tile key w*32*kItems + k*32 + l)
+  uint32_t* wh = whist + w * kWhistStride;
   const uint32_t lt = lanemask_lt();
 #pragma unroll
   for (int k = 0; k < kItems; ++k) {
-    const uint64_t i = t0 + w * (32 * kItems) + k * 32 + lane;
-    key[k] = i < n ? kin[i] : ~0ull;
-  }
-#pragma unroll
-  for (int k = 0; k < kItems; ++k) {
-    const uint64_t i = t0 + w * (32 * kItems) + k * 32 + lane;
-    const uint32_t d = i < n ? static_cast<uint32_t>(key[k] >> shift) & 0xffu : static_cast<uint32_t>(kBins);
-    const uint32_t peers = __match_any_sync(kFullMask, d);
+    const uint32_t j = static_cast<uint32_t>(w * (32 * kItems) + k * 32 + lane);
+    const uint32_t d = j < tn ? static_cast<uint32_t>(key[k] >> shift) & 0xffu : static_cast<uint32_t>(kBins);
+    const uint32_t peers = peers_of(d);
     const uint32_t before = wh[d];
     __syncwarp();
     rank[k] = before + __popc(peers & lt);
@@ -185,30 +246,27 @@ __global__ void __launch_bounds__(kSortThreads) sort_pass_kernel(PassBufs bufs, 
   uint32_t cnt = 0;
 #pragma unroll
   for (int v = 0; v < kSortWarps; ++v) {
-    const uint32_t c = whist[v * (kBins + 1) + d];
-    whist[v * (kBins + 1) + d] = cnt;
+    const uint32_t c = whist[v * kWhistStride + d];
+    whist[v * kWhistStride + d] = cnt;
     cnt += c;
   }
   const uint64_t epoch = static_cast<uint64_t>(byte + 1) << 40;
   volatile uint64_t* st = status;
   if (tile == 0) st[d] = kFlagPrefix | epoch | cnt;
   else st[tile * kBins + d] = kFlagAgg | epoch | cnt;
-  // tile-local exclusive scan over the digits
-  uint32_t incl = cnt;
+  uint32_t incl = cnt;  // tile-local exclusive scan over the digits
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t v = __shfl_up_sync(kFullMask, incl, o);
     if (lane >= o) incl += v;
   }
-  __shared__ uint32_t wsum[kSortWarps];
   if (lane == 31) wsum[w] = incl;
   __syncthreads();
   uint32_t wpre = 0;
 #pragma unroll
   for (int v = 0; v < kSortWarps; ++v) wpre += v < w ? wsum[v] : 0u;
   loff[d] = wpre + incl - cnt;
-  // decoupled look-back for this digit's offset among earlier tiles
-  uint64_t excl = 0;
+  uint64_t excl = 0;  // decoupled look-back: this digit's offset among earlier tiles
   if (tile > 0) {
     for (int64_t p = static_cast<int64_t>(tile) - 1; p >= 0; --p) {
       uint64_t s;
@@ -221,51 +279,80 @@ __global__ void __launch_bounds__(kSortThreads) sort_pass_kernel(PassBufs bufs, 
     st[tile * kBins + d] = kFlagPrefix | epoch | (excl + cnt);
   }
   gbase[d] = ctl->hist[byte][d] + excl;
+  if (!first) cp_async_wait_all();
   __syncthreads();
 
-  // ---- stage the tile in digit order, then write each digit's run contiguously
+  // ---- stage the tile in digit order
 #pragma unroll
   for (int k = 0; k < kItems; ++k) {
     const uint32_t j = static_cast<uint32_t>(w * (32 * kItems) + k * 32 + lane);
-    if (t0 + j < n) {
+    if (j < tn) {
       const uint32_t dg = static_cast<uint32_t>(key[k] >> shift) & 0xffu;
-      const uint32_t pos = loff[dg] + whist[w * (kBins + 1) + dg] + rank[k];
+      const uint32_t pos = loff[dg] + whist[w * kWhistStride + dg] + rank[k];
       LC_CHECK(pos < static_cast<uint32_t>(kTileKeys));
       skeys[pos] = key[k];
-      srows[pos] = first ? static_cast<uint32_t>(t0 + j) : rin[t0 + j];
+      srows[pos] = first ? static_cast<uint32_t>(t0 + j) : irows[j];
     }
   }
   __syncthreads();
-  const uint32_t tn = static_cast<uint32_t>(n - t0 < static_cast<uint64_t>(kTileKeys) ? n - t0 : kTileKeys);
-  uint64_t* __restrict__ kout = bufs.keys[ib ^ 1u];
-  uint32_t* __restrict__ rout = bufs.rows[ib ^ 1u];
-  for (uint32_t j = tid; j < tn; j += kSortThreads) {
-    const uint64_t k = skeys[j];
-    const uint32_t dg = static_cast<uint32_t>(k >> shift) & 0xffu;
-    const uint64_t o = gbase[dg] + (j - loff[dg]);
-    LC_CHECK(o < n && j >= loff[dg]);
-    kout[o] = k;
-    rout[o] = srows[j];
+
+  // ---- write each digit's run contiguously; the last pass gathers the payload columns
+  if (!last) {
+    const uint32_t ob = first ? 1u - (ctl->passes & 1u) : ib ^ 1u;  // (passes - 1) & 1 for pass 0
+    uint64_t* __restrict__ kout = bufs.keys[ob];
+    uint32_t* __restrict__ rout = bufs.rows[ob];
+    for (uint32_t j = tid; j < tn; j += kSortThreads) {
+      const uint64_t k = skeys[j];
+      const uint32_t dg = static_cast<uint32_t>(k >> shift) & 0xffu;
+      const uint64_t o = gbase[dg] + (j - loff[dg]);
+      LC_CHECK(o < n && j >= loff[dg]);
+      kout[o] = k;
+      rout[o] = srows[j];
+    }
+  } else {
+    uint64_t* __restrict__ kout = cols.out[0];
+    constexpr int U = 4;  // records per thread per round: U payload sectors in flight
+    for (uint32_t j0 = tid; j0 < tn; j0 += kSortThreads * U) {
+      uint64_t o[U];
+      ulonglong2 a[U], b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t j = j0 + u * kSortThreads;
+        if (j < tn) {
+          const uint64_t k = skeys[j];
+          const uint32_t dg = static_cast<uint32_t>(k >> shift) & 0xffu;
+          o[u] = gbase[dg] + (j - loff[dg]);
+          LC_CHECK(o[u] < n && j >= loff[dg]);
+          kout[o[u]] = k;
+          const uint64_t r = srows[j];
+          a[u] = aos[2 * r];
+          b[u] = aos[2 * r + 1];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t j = j0 + u * kSortThreads;
+        if (j < tn) {
+          if (cols.out[1]) cols.out[1][o[u]] = a[u].x;
+          if (cols.out[2]) cols.out[2][o[u]] = a[u].y;
+          if (cols.out[3]) cols.out[3][o[u]] = b[u].x;
+          if (cols.out[4]) cols.out[4][o[u]] = b[u].y;
+        }
+      }
+    }
   }
 }
 
-// out[c][i] = in[c][row[i]] for the payload columns; keys from the final buffer.
-__global__ void sort_gather_kernel(PassBufs bufs, uint64_t n, const SortCtl* ctl, Cols cols, int ncols) {
-  const uint32_t fb = ctl->final_buf;
-  const bool none = ctl->passes == 0u;  // already ascending: a copy
-  const uint64_t* __restrict__ keys = none ? bufs.kfirst : bufs.keys[fb];
-  const uint32_t* __restrict__ rows = bufs.rows[fb];
+// Already ascending (no pass runs): the output columns are a copy of the input.
+__global__ void sort_copy_kernel(uint64_t n, const SortCtl* ctl, Cols cols) {
+  if (ctl->passes != 0u) return;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t r = none ? i : rows[i];
-    if (keys != cols.out[0]) cols.out[0][i] = keys[i];
 #pragma unroll
-    for (int c = 1; c < 5; ++c)
-      if (c < ncols && cols.in[c]) cols.out[c][i] = cols.in[c][r];
+    for (int c = 0; c < kCols; ++c)
+      if (cols.in[c]) cols.out[c][i] = cols.in[c][i];
   }
 }
-
-constexpr size_t kPassSmem = kTileKeys * (8 + 4) + (kSortWarps * (kBins + 1) + 1) * 4 + kBins * 8 + kBins * 4 + 16;
 
 inline size_t align256(size_t b) { return (b + 255) & ~size_t{255}; }
 
@@ -273,15 +360,16 @@ inline size_t align256(size_t b) { return (b + 255) & ~size_t{255}; }
 
 size_t radix_sort_scratch_bytes(uint64_t n) {
   const uint64_t tiles = (n + kTileKeys - 1) / kTileKeys;
-  return align256(sizeof(SortCtl)) + align256(n * 8) + 2 * align256(n * 4) + align256(tiles * kBins * 8);
+  return align256(sizeof(SortCtl)) + align256(n * 8) + 2 * align256(n * 4) + align256(tiles * kBins * 8) +
+         align256(n * 32);
 }
 
-// cols_in[0] is the key column; out-of-place (cols_out[c] must not alias any cols_in);
+// cols_in[0] is the key column; out of place (cols_out[c] must not alias any cols_in);
 // null payload columns are skipped.  Rows are 32-bit: n < 2^32.  Enqueued without a host
 // synchronisation.
 cudaError_t radix_sort_records(uint64_t n, const uint64_t* const* cols_in, uint64_t* const* cols_out, int ncols,
                                void* scratch, size_t scratch_bytes, cudaStream_t st, int* launches) {
-  if (n >= (1ull << 32) || ncols < 1 || ncols > 5) return cudaErrorInvalidValue;
+  if (n >= (1ull << 32) || ncols < 1 || ncols > kCols) return cudaErrorInvalidValue;
   if (scratch_bytes < radix_sort_scratch_bytes(n)) return cudaErrorInvalidValue;
   if (n == 0) return cudaSuccess;
   uint8_t* p = static_cast<uint8_t*>(scratch);
@@ -295,12 +383,14 @@ cudaError_t radix_sort_records(uint64_t n, const uint64_t* const* cols_in, uint6
   p += align256(n * 4);
   const uint64_t tiles = (n + kTileKeys - 1) / kTileKeys;
   uint64_t* status = reinterpret_cast<uint64_t*>(p);
+  p += align256(tiles * kBins * 8);
+  ulonglong2* aos = reinterpret_cast<ulonglong2*>(p);
   cudaError_t e;
   if ((e = cudaMemsetAsync(ctl, 0, sizeof(SortCtl), st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(status, 0, tiles * kBins * 8, st)) != cudaSuccess) return e;
-  PassBufs bufs{cols_in[0], {cols_out[0], kbuf}, {r0, r1}};
+  PassBufs bufs{{cols_out[0], kbuf}, {r0, r1}};
   Cols cols{};
-  for (int c = 0; c < 5; ++c) {
+  for (int c = 0; c < kCols; ++c) {
     cols.in[c] = c < ncols ? cols_in[c] : nullptr;
     cols.out[c] = c < ncols ? cols_out[c] : nullptr;
   }
@@ -308,15 +398,15 @@ cudaError_t radix_sort_records(uint64_t n, const uint64_t* const* cols_in, uint6
   if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
   if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
   const uint64_t hb = std::min<uint64_t>((n + kSortThreads - 1) / kSortThreads, static_cast<uint64_t>(sms) * 8);
-  sort_hist_kernel<<<static_cast<unsigned>(hb), kSortThreads, 0, st>>>(cols_in[0], n, ctl);
+  sort_hist_kernel<<<static_cast<unsigned>(hb), kSortThreads, 0, st>>>(cols_in[0], n, ctl, cols, aos);
   sort_plan_kernel<<<1, kBins, 0, st>>>(n, ctl);
   if ((e = cudaFuncSetAttribute(sort_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(kPassSmem))) != cudaSuccess)
     return e;
   for (int b = 0; b < kBytes; ++b)  // trivial bytes return at once (decided on the device)
-    sort_pass_kernel<<<static_cast<unsigned>(tiles), kSortThreads, kPassSmem, st>>>(bufs, n, b, ctl, status);
-  const uint64_t gb = std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(sms) * 16);
-  sort_gather_kernel<<<static_cast<unsigned>(gb), 256, 0, st>>>(bufs, n, ctl, cols, ncols);
+    sort_pass_kernel<<<static_cast<unsigned>(tiles), kSortThreads, kPassSmem, st>>>(bufs, cols, n, b, ctl, status, aos);
+  const uint64_t gb = std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(sms) * 8);
+  sort_copy_kernel<<<static_cast<unsigned>(gb), 256, 0, st>>>(n, ctl, cols);
   *launches += 3 + kBytes;
   return cudaGetLastError();
 }
