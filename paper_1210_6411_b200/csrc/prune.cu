@@ -306,7 +306,8 @@ template <class S, int R, bool DFS>
 __device__ __forceinline__ int prune_step_unified(const uint8_t* tbl, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t& d,
                                            uint64_t& acc, bool& climb, Pending<R>& pend, uint32_t F,
                                            uint64_t limit) {
-  uint64_t enode;
+  // the entry's node is held in r1..r3 (packed only when its remaining children go to the
+  // pending set, unpacked only when a leaf resumes a pending entry)
   uint32_t edm;
   if (climb) {
     // the parent y of the current node: continue with the next-lower sibling, else y's
@@ -324,12 +325,11 @@ __device__ __forceinline__ int prune_step_unified(const uint8_t* tbl, uint32_t& 
     if (lower == 0u) {  // y's subtree is done as well
       const int r = resume_or_finish<S, R>(d, climb, pend);
       if (r != 0 || climb) return r;
-      enode = pend.cnode;
+      unpack2<S>(pend.cnode, r1, r2, r3);
       edm = pend.cdm;
       pend.cdm = 0u;
     } else {
       climb = false;
-      enode = y;
       edm = (d << 4) | lower;
     }
   } else {
@@ -348,12 +348,11 @@ __device__ __forceinline__ int prune_step_unified(const uint8_t* tbl, uint32_t& 
           return 2;
         }
       }
-      enode = pack2<S>(r1, r2, r3);
       edm = (d << 4) | m;
     } else {
       const int r = resume_or_finish<S, R>(d, climb, pend);
       if (r != 0 || climb) return r;
-      enode = pend.cnode;
+      unpack2<S>(pend.cnode, r1, r2, r3);
       edm = pend.cdm;
       pend.cdm = 0u;  // taken out of the cache (the rest goes back below)
     }
@@ -362,8 +361,7 @@ __device__ __forceinline__ int prune_step_unified(const uint8_t* tbl, uint32_t& 
   const uint32_t q = 31 - __clz(mask);  // the LIFO stack pops the last-pushed (highest) child first
   const uint32_t rest = mask & ~(1u << q);
   const uint32_t ed = edm >> 4;
-  if (rest) pend.push(enode, ed, rest);
-  unpack2<S>(enode, r1, r2, r3);
+  if (rest) pend.push(pack2<S>(r1, r2, r3), ed, rest);
   d = ed + 1;
   child2<S>(r1, r2, r3, q);
   return 0;
@@ -383,8 +381,11 @@ __device__ __forceinline__ int prune_step2(const uint8_t* tbl, uint32_t& r1, uin
 #endif
 }
 
+#ifndef LC_PRUNE2_MINBLOCKS
+#define LC_PRUNE2_MINBLOCKS 1
+#endif
 template <class S, int R, bool DFS>
-__global__ void __launch_bounds__(kThreads2) prune2_kernel(const uint64_t* __restrict__ cands, uint64_t n, uint32_t F,
+__global__ void __launch_bounds__(kThreads2, LC_PRUNE2_MINBLOCKS) prune2_kernel(const uint64_t* __restrict__ cands, uint64_t n, uint32_t F,
                                                            uint64_t limit, uint8_t* __restrict__ removed,
                                                            uint64_t* __restrict__ work, unsigned long long* queue,
                                                            uint64_t* spill_node, uint16_t* spill_dm,
