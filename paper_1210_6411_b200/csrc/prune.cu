@@ -367,14 +367,91 @@ __device__ __forceinline__ int prune_step_unified(const uint8_t* tbl, uint32_t& 
   return 0;
 }
 
+// The unified step with the pending-set traffic flattened: per step a lane does at most
+// one shared-memory ring access -- a pop when a leaf finds the register cache empty, or a
+// demotion of the cache when a node with several children needs it -- written as
+// predicated straight-line code, so a warp issues it once for all its lanes instead of
+// once per divergent branch (ncu: a quarter of the warp instructions of the branchy form
+// ran with at most 3 of 32 lanes active).  The rare cases (spill refill, end of the
+// traversal, climbing) keep their branches.
+template <class S, int R, bool DFS>
+__device__ __forceinline__ int prune_step_flat(const uint8_t* tbl, uint32_t& r1, uint32_t& r2, uint32_t& r3,
+                                               uint32_t& d, uint64_t& acc, bool& climb, Pending<R>& pend,
+                                               uint32_t F, uint64_t limit) {
+  if (climb) return prune_step_unified<S, R, DFS>(tbl, r1, r2, r3, d, acc, climb, pend, F, limit);
+  const uint32_t m = child_set<S>(tbl, r1, r2, r3, F);
+  const bool leaf = m == 0u;
+  if (!leaf) {
+    if (DFS) {
+      if (d >= limit) {  // a child would sit below the depth limit (pipeline.py:138-141)
+        acc += 1;
+        return 2;
+      }
+      acc += __popc(m);
+    } else {
+      acc += __popc(m);
+      if (acc > limit) {  // pipeline.py:155-157
+        acc = limit + 1;
+        return 2;
+      }
+    }
+  } else if (d > kDepthCap2 || (pend.cdm == 0u && pend.cnt == 0u)) {
+    // leaf with nothing cached or in the shared ring: spill refill, climb or done
+    const int r = resume_or_finish<S, R>(d, climb, pend);
+    if (r != 0 || climb) return r;
+  }
+  // ring pop: a leaf whose cache is empty takes the ring's newest entry (cnt > 0 here)
+  const bool pop = leaf && pend.cdm == 0u;
+  const uint32_t a = pend.at(pend.top);
+  uint64_t rn = pend.cnode;
+  uint32_t rdm = pend.cdm;
+  if (pop) {
+    rn = pend.node[a];
+    rdm = pend.dm[a];
+    pend.top = pend.top == 0u ? R - 1 : pend.top - 1;
+    --pend.cnt;
+  }
+  uint32_t edm = (d << 4) | m;
+  if (leaf) {
+    unpack2<S>(rn, r1, r2, r3);
+    edm = rdm;
+    pend.cdm = 0u;
+  }
+  const uint32_t mask = edm & 15u;
+  const uint32_t q = 31 - __clz(mask);  // the LIFO stack pops the last-pushed (highest) child first
+  const uint32_t rest = mask & ~(1u << q);
+  const uint32_t ed = edm >> 4;
+  if (rest && ed < kDepthCap2) {  // deeper entries are found again by climbing
+    if (pend.cdm) {  // demote the cache into the ring (its oldest entry to the spill when full)
+      if (pend.cnt == static_cast<uint32_t>(R)) {
+        pend.demote();
+      } else {
+        const uint32_t nt = pend.top + 1 == static_cast<uint32_t>(R) ? 0u : pend.top + 1;
+        const uint32_t b = pend.at(nt);
+        pend.node[b] = pend.cnode;
+        pend.dm[b] = static_cast<uint16_t>(pend.cdm);
+        pend.top = nt;
+        ++pend.cnt;
+      }
+    }
+    pend.cnode = pack2<S>(r1, r2, r3);
+    pend.cdm = (ed << 4) | rest;
+  }
+  d = ed + 1;
+  child2<S>(r1, r2, r3, q);
+  return 0;
+}
+
 #ifndef LC_PRUNE2_UNIFIED
-#define LC_PRUNE2_UNIFIED 1  // 0: the two-path step (A/B)
+#define LC_PRUNE2_UNIFIED 1  // 0: the two-path step, 2: flattened ring traffic (A/B)
 #endif
 template <class S, int R, bool DFS>
 __device__ __forceinline__ int prune_step2(const uint8_t* tbl, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t& d,
                                            uint64_t& acc, bool& climb, Pending<R>& pend, uint32_t F,
                                            uint64_t limit) {
-#if LC_PRUNE2_UNIFIED
+#if LC_PRUNE2_UNIFIED == 2
+  return prune_step_flat<S, R, DFS>(tbl, r1, r2, r3, d, acc, climb, pend, F, limit);
+#elif LC_PRUNE2_UNIFIED
   return prune_step_unified<S, R, DFS>(tbl, r1, r2, r3, d, acc, climb, pend, F, limit);
 #else
   return prune_step_split<S, R, DFS>(tbl, r1, r2, r3, d, acc, climb, pend, F, limit);

@@ -40,7 +40,13 @@ namespace {
 constexpr uint32_t kFullMask = 0xffffffffu;
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kItems = 12;                          // keys per thread
+#ifndef LC_SORT_ITEMS
+#define LC_SORT_ITEMS 12
+#endif
+#ifndef LC_SORT_MINBLOCKS
+#define LC_SORT_MINBLOCKS 3
+#endif
+constexpr int kItems = LC_SORT_ITEMS;               // keys per thread
 constexpr int kTileKeys = kSortThreads * kItems;    // 3072
 constexpr int kBins = 256;
 constexpr int kBytes = 8;
@@ -183,7 +189,7 @@ constexpr int kWhistStride = kBins + 1;  // one spare counter per warp for lanes
 constexpr size_t kSmemKeys = kTileKeys * 8, kSmemRows = kTileKeys * 4;
 constexpr size_t kPassSmem = kSmemKeys + 2 * kSmemRows + (kSortWarps * kWhistStride + 8) * 4 + kBins * 8 + kBins * 4;
 
-__global__ void __launch_bounds__(kSortThreads, 3) sort_pass_kernel(PassBufs bufs, Cols cols, uint64_t n, int byte,
+__global__ void __launch_bounds__(kSortThreads, LC_SORT_MINBLOCKS) sort_pass_kernel(PassBufs bufs, Cols cols, uint64_t n, int byte,
                                                                     SortCtl* ctl, uint64_t* status,
                                                                     const ulonglong2* __restrict__ aos) {
   if (ctl->trivial[byte]) return;
