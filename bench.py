@@ -357,15 +357,17 @@ def main() -> None:
     per_launch_tr = local_summ["transitions"] / max(args.steps, 1)
     achieved = per_launch_tr * LOP3_PER_TRANSITION / (sum(kernel_s) / len(kernel_s))
 
-    # ---- parity (untimed): batches the timed steps did not reach are walked now, then
-    # every batch of this rank is hashed; rank 0's seed-0 stream has committed digests
-    for b in range(min(args.steps, nbatches), nbatches):
+    # ---- parity (untimed): batches of this rank's first 2^24-start stream that the timed
+    # steps did not reach are walked now, then that stream is hashed; rank 0's seed-0
+    # stream (config 2) has committed digests
+    checked = min(per_gpu, STREAM)
+    for b in range(min(args.steps, nbatches), min(nbatches, max(1, checked // batch))):
         walk(b, wstats)
     torch.cuda.synchronize()
     parity = None
     if args.starts == "ref" and LEGS == 1 and STRIDE_ == STRIDE:
-        h_dst = dst.cpu().numpy().view(np.uint64)
-        h_dist = dist_.cpu().numpy().view(np.uint64)
+        h_dst = dst[:checked].cpu().numpy().view(np.uint64)
+        h_dist = dist_[:checked].cpu().numpy().view(np.uint64)
         parity = {"edge_digest": batch_digest(h_dst, h_dist), "walks_hashed": int(h_dst.size)}
         if seeds[0] == 0 and per_gpu >= STREAM:
             c1 = load_json(os.path.join(GOLDEN, "a51_c1_65536.json"))

@@ -18,13 +18,17 @@
  *    are ordered on the device: each call's stream first waits for the previous call's
  *    work (an event the context records), so `_device` calls on different streams may
  *    share a context safely; they then run one after another, not concurrently.
- *  - Only the three built-in ciphers (A5/1, mini567, mini789 -- cipher.py:173-194) have
- *    compiled kernels; any other spec returns LC_ERR_UNSUPPORTED (there is no CPU path).
+ *  - The three built-in ciphers (A5/1, mini567, mini789 -- cipher.py:173-194) have
+ *    precompiled kernels; any other valid spec (registers of at most 32 bits) gets the
+ *    same kernels compiled for it at first use (NVRTC, csrc/jit.cu).  Specs the kernels
+ *    cannot hold return LC_ERR_UNSUPPORTED (there is no CPU path).
  */
 #ifndef LFSR_B200_H
 #define LFSR_B200_H
 
+#ifndef __CUDACC_RTC__
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -35,7 +39,7 @@ extern "C" {
 #define LC_OK 0
 #define LC_ERR_ARG (-1)          /* ValueError in the reference (bitslice.py:269-272, ...) */
 #define LC_ERR_CUDA (-2)         /* CUDA runtime failure */
-#define LC_ERR_UNSUPPORTED (-3)  /* spec without a compiled kernel */
+#define LC_ERR_UNSUPPORTED (-3)  /* spec the kernels cannot hold (or NVRTC unavailable) */
 #define LC_ERR_CAP (-4)          /* StrideError: walk cap exceeded (bitslice.py:316-322) */
 #define LC_ERR_INVALID_STATE (-5)/* a start has a zero register; the reference
                                     walks it to the cap and raises StrideError */

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "liblfsr_b200.so")
-SOURCES = ["walk.cu", "kernels.cu", "peak.cu", "reduce.cu", "bruteforce.cu", "sampler.cu", "prune.cu", "sort.cu", "capi.cu"]
+SOURCES = ["walk.cu", "kernels.cu", "peak.cu", "reduce.cu", "bruteforce.cu", "sampler.cu", "prune.cu", "sort.cu", "jit.cu", "capi.cu"]
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-cudart", "static",
               "--expt-relaxed-constexpr"]
@@ -54,7 +54,7 @@ def _compile(out_dir: str, lib: str, defines: list, verbose: bool) -> str:
         if proc.wait() != 0:
             raise subprocess.CalledProcessError(proc.returncode, cmd)
     tmp = lib + ".tmp"
-    subprocess.run([nvcc(), *GENCODE, "-shared", "-cudart", "static", "-o", tmp, *objs], check=True)
+    subprocess.run([nvcc(), *GENCODE, "-shared", "-cudart", "static", "-o", tmp, *objs, "-ldl"], check=True)
     os.replace(tmp, lib)
     return lib
 

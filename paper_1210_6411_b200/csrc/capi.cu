@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "jit.h"
 #include "lfsr_internal.h"
 
 namespace {
@@ -94,13 +95,32 @@ uint32_t default_fixed(lc::SpecId id) {
   }
 }
 
-int l3_of(lc::SpecId id) { return id == lc::SpecId::A51 ? 23 : (id == lc::SpecId::MINI567 ? 7 : 9); }
+int l3_of(lc::SpecId id) {
+  if (id == lc::SpecId::CUSTOM) return lc::current_custom() ? lc::current_custom()->lengths[2] : 0;
+  return id == lc::SpecId::A51 ? 23 : (id == lc::SpecId::MINI567 ? 7 : 9);
+}
 
+uint32_t r3_taps(lc::SpecId id) {
+  switch (id) {
+    case lc::SpecId::A51: return (1u << 7) | (1u << 20) | (1u << 21) | (1u << 22);
+    case lc::SpecId::MINI567: return (1u << 5) | (1u << 6);
+    case lc::SpecId::MINI789: return (1u << 3) | (1u << 8);
+    case lc::SpecId::CUSTOM: return lc::current_custom() ? static_cast<uint32_t>(lc::current_custom()->taps[2]) : 0u;
+    default: return 0u;
+  }
+}
+
+// A built-in spec, or a valid custom one: its kernels are compiled for it at first use
+// (csrc/jit.cu) and become the calling thread's current custom spec.
 int check_spec(const lc_spec* spec, lc::SpecId* id) {
   *id = identify(spec);
-  if (*id == lc::SpecId::UNSUPPORTED)
-    return fail(LC_ERR_UNSUPPORTED,
-                "no compiled kernel for this cipher spec (built-ins: a51, mini567, mini789)");
+  if (*id != lc::SpecId::UNSUPPORTED) return LC_OK;
+  if (!spec) return fail(LC_ERR_ARG, "null spec");
+  std::string err;
+  const lc::CustomKernels* k = lc::custom_kernels_for(spec, &err);
+  if (!k) return fail(LC_ERR_UNSUPPORTED, "custom cipher spec: %s", err.c_str());
+  lc::set_current_custom(k);
+  *id = lc::SpecId::CUSTOM;
   return LC_OK;
 }
 
@@ -108,6 +128,13 @@ int check_fixed(lc::SpecId id, uint64_t fixed_r3) {
   const int l3 = l3_of(id);
   if (fixed_r3 == 0 || fixed_r3 >= (1ull << l3))
     return fail(LC_ERR_ARG, "fixed R3 value must be a nonzero %d-bit value", l3);
+  if (id == lc::SpecId::CUSTOM) {
+    // the kernels take "R3 clocked" for "R3 leaves F"; that fails only if F is a fixed
+    // point of R3's step, and then no state is a special node at all
+    const uint32_t m = l3 >= 32 ? ~0u : (1u << l3) - 1u, f = static_cast<uint32_t>(fixed_r3);
+    const uint32_t next = ((f << 1) & m) | (static_cast<uint32_t>(__builtin_popcount(f & r3_taps(id))) & 1u);
+    if (next == f) return fail(LC_ERR_ARG, "fixed R3 value is a fixed point of R3's step: there are no special nodes");
+  }
   return LC_OK;
 }
 
@@ -121,6 +148,9 @@ struct lc_ctx {
   int mapped_sms = -1;  // SMs found by the %smid probe (-1: not probed yet)
   int need3_id = -1;    // spec / fixed R3 the need3 table was built for
   uint64_t need3_f = 0;
+  const void* need3_custom = nullptr;  // (custom spec)
+  bool need3_valid = false;            // a table exists (custom specs with l3 > 24 have none)
+  uint64_t window = 0;                 // R3's period through F (WalkParams::window)
   cudaEvent_t done = nullptr;  // recorded after the last call's work (see Ordered)
 };
 
@@ -161,29 +191,44 @@ int ensure_smsp_map(lc_ctx* ctx) {
 }
 
 // need3[v] = R3 clocks from R3 value v to the fixed value F (the walk's arming bound):
-// one pass over R3's maximal-period sequence starting at F, built once per (spec, F).
+// one pass over R3's sequence starting at F, built once per (spec, F).  Its length is R3's
+// period through F (2^l3 - 1 for maximal-period registers), the walk's check-free
+// window.  Values off F's cycle (custom specs with non-maximal R3) never reach F:
+// UINT32_MAX, so those lanes run to the cap audit like the reference's (StrideError).
 int ensure_need3(lc_ctx* ctx, lc::SpecId id, uint64_t F) {
-  if (ctx->need3_id == static_cast<int>(id) && ctx->need3_f == F) return LC_OK;
-  int l3;
-  uint32_t taps;
-  switch (id) {
-    case lc::SpecId::A51: l3 = 23; taps = (1u << 7) | (1u << 20) | (1u << 21) | (1u << 22); break;
-    case lc::SpecId::MINI567: l3 = 7; taps = (1u << 5) | (1u << 6); break;
-    case lc::SpecId::MINI789: l3 = 9; taps = (1u << 3) | (1u << 8); break;
-    default: return fail(LC_ERR_UNSUPPORTED, "no R3 table for this spec");
-  }
-  const uint32_t mask = (1u << l3) - 1u, period = mask;
-  std::vector<uint32_t> need(static_cast<size_t>(mask) + 1u, 0u);
+  const void* custom = id == lc::SpecId::CUSTOM ? static_cast<const void*>(lc::current_custom()) : nullptr;
+  if (ctx->need3_id == static_cast<int>(id) && ctx->need3_f == F && ctx->need3_custom == custom) return LC_OK;
+  const int l3 = l3_of(id);
+  const uint32_t taps = r3_taps(id);
+  if (l3 < 2 || !taps) return fail(LC_ERR_UNSUPPORTED, "no R3 table for this spec");
+  const uint32_t mask = l3 >= 32 ? ~0u : (1u << l3) - 1u;
+  auto step = [&](uint32_t x) { return ((x << 1) & mask) | (static_cast<uint32_t>(__builtin_popcount(x & taps)) & 1u); };
+  const bool table = l3 <= 24;
+  std::vector<uint32_t> need(table ? static_cast<size_t>(mask) + 1u : 0u, ~0u);
+  uint64_t period = 0;
   uint32_t x = static_cast<uint32_t>(F);
-  for (uint32_t k = 0; k < period; ++k) {
-    need[x] = (period - k) % period;
-    x = ((x << 1) & mask) | (static_cast<uint32_t>(__builtin_popcount(x & taps)) & 1u);
+  if (l3 <= 28) {
+    do {
+      x = step(x);
+      ++period;
+    } while (x != F);
+  } else {
+    period = 1;  // too long to trace here: check every clock (correct, slower)
   }
-  if (x != F) return fail(LC_ERR_UNSUPPORTED, "R3 is not a maximal-period register");
-  LC_CUDA(ctx->need3.ensure(need.size() * 4));
-  LC_CUDA(cudaMemcpy(ctx->need3.p, need.data(), need.size() * 4, cudaMemcpyHostToDevice));
+  if (table) {
+    x = static_cast<uint32_t>(F);
+    for (uint64_t k = 0; k < period; ++k) {
+      need[x] = static_cast<uint32_t>((period - k) % period);
+      x = step(x);
+    }
+    LC_CUDA(ctx->need3.ensure(need.size() * 4));
+    LC_CUDA(cudaMemcpy(ctx->need3.p, need.data(), need.size() * 4, cudaMemcpyHostToDevice));
+  }
   ctx->need3_id = static_cast<int>(id);
   ctx->need3_f = F;
+  ctx->need3_custom = custom;
+  ctx->need3_valid = table;
+  ctx->window = period;
   return LC_OK;
 }
 
@@ -349,7 +394,8 @@ int walk_launch(lc_ctx* ctx, const WalkArgs& a, const uint64_t* d_starts, const 
   p.park_below = pool ? park_below : 0u;
   p.n_dev = n_dev;
   p.park_min = park_min;
-  p.need3 = ctx->need3.as<uint32_t>();
+  p.need3 = ctx->need3_valid ? ctx->need3.as<uint32_t>() : nullptr;
+  p.window = ctx->window;
   p.run_if_mode = ~0u;
   // Re-arming pays for lanes that would otherwise be checked for long stretches: lane
   // mode (independent lanes), or any walk whose stride is below R3's period.  Whole-warp
@@ -635,6 +681,9 @@ int lc_random_candidates_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed
   LC_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
   Ordered ord_(ctx, st);
+  if (id == lc::SpecId::CUSTOM)
+    return fail(LC_ERR_UNSUPPORTED, "the K0 generator is built for the built-in ciphers only "
+                                    "(lc_reference_candidates serves any spec)");
   uint64_t trials = static_cast<uint64_t>(static_cast<double>(n) / acceptance_estimate(id)) + 65536;
   for (int attempt = 0; attempt < 8; ++attempt) {
     const uint64_t words = lc::random_scratch_words(trials);
@@ -697,7 +746,7 @@ int lc_prune_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int32_t
   uint32_t spill_cap = LC_PRUNE_SPILL;
   if (const char* env = getenv("LFSR_PRUNE_SPILL")) spill_cap = static_cast<uint32_t>(strtoul(env, nullptr, 10));
   const char* v1 = getenv("LFSR_PRUNE_V1");  // A/B: the round-1 kernel (64-bit node, no register cache)
-  if (v1 && v1[0] == '1') {
+  if (v1 && v1[0] == '1' && id != lc::SpecId::CUSTOM) {
     const int ring = lc::prune_ring_for(n);
     const int blocks = lc::prune_blocks_per_sm(id, ring) * ctx->sms;
     if (spill_cap) LC_CUDA(ctx->spill.ensure(lc::prune_spill_bytes(blocks, spill_cap)));
@@ -1000,6 +1049,7 @@ int lc_bf_build_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int 
   int rc = check_spec(spec, &id);
   if (rc) return rc;
   if ((rc = check_fixed(id, fixed_r3))) return rc;
+  if (id == lc::SpecId::CUSTOM) return fail(LC_ERR_UNSUPPORTED, "the exhaustive analysis is built for the minis only");
   if (n != valid_states(id)) return fail(LC_ERR_ARG, "n must be the spec's valid state count");
   if (n > (1ull << 31)) return fail(LC_ERR_ARG, "instance too large for exhaustive analysis");
   if (!d_succ || !d_indeg || !d_is_cand || !d_cycle_of) return fail(LC_ERR_ARG, "null buffer");

@@ -3,12 +3,17 @@
 // enumeration of step 1 (K2, pipeline.enumerate_candidates), the seeded start-set
 // generator (K0, ordered compaction), the step-2 prune (K3,
 // pipeline.prune_shallow_segments) and the closure check of build_skeleton_edges.
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#endif
 
 #include "lfsr_common.cuh"
 #include "lfsr_internal.h"
+#ifndef __CUDACC_RTC__
+#include "jit.h"
+#endif
 
 namespace lc {
 
@@ -173,6 +178,7 @@ __global__ void __launch_bounds__(kCompactThreads) compact_write_kernel(Gen g, u
   }
 }
 
+#ifndef __CUDACC_RTC__
 template <class S, class Gen>
 cudaError_t compact(Gen g, uint64_t total, uint32_t F, uint64_t* out, uint64_t cap, uint64_t* d_count,
                     uint64_t* scratch, cudaStream_t stream, int* launches) {
@@ -188,6 +194,7 @@ cudaError_t compact(Gen g, uint64_t total, uint32_t F, uint64_t* out, uint64_t c
   if (launches) *launches += 3;
   return cudaGetLastError();
 }
+#endif
 
 // ---------------------------------------------------------------- K2: step-1 enumeration
 // On the fixed-R3 plane the special-node predicate (cipher.py:420-428) depends only on
@@ -673,12 +680,17 @@ __global__ void first_missing_kernel(const uint64_t* __restrict__ set, uint64_t 
   }
 }
 
+#ifndef __CUDACC_RTC__
 inline unsigned grid_for(uint64_t n, int threads, uint64_t per_thread = 1) {
   const uint64_t g = (n + static_cast<uint64_t>(threads) * per_thread - 1) / (static_cast<uint64_t>(threads) * per_thread);
   return static_cast<unsigned>(g == 0 ? 1 : (g > (1u << 20) ? (1u << 20) : g));
 }
 
+#endif
+
 }  // namespace
+
+#ifndef __CUDACC_RTC__
 
 #define LC_DISPATCH(id, ...)                                  \
   switch (id) {                                               \
@@ -688,14 +700,24 @@ inline unsigned grid_for(uint64_t n, int threads, uint64_t per_thread = 1) {
     default: return cudaErrorInvalidValue;                    \
   }
 
+// SpecId::CUSTOM: the calling thread's runtime-compiled kernels (csrc/jit.cu)
+#define LC_CUSTOM_OR(id)                              \
+  const CustomKernels* custom = current_custom();     \
+  if ((id) == SpecId::CUSTOM && !custom) return cudaErrorInvalidValue;
+
 cudaError_t launch_is_candidate(SpecId id, const uint64_t* xs, uint64_t n, uint32_t F, uint8_t* out,
                                 cudaStream_t stream) {
+  LC_CUSTOM_OR(id)
+  if (id == SpecId::CUSTOM) return jit_launch(custom->is_candidate, grid_for(n, kThreads), kThreads, 0, stream, xs, n, F, out);
   LC_DISPATCH(id, is_candidate_kernel<S><<<grid_for(n, kThreads), kThreads, 0, stream>>>(xs, n, F, out);
               return cudaGetLastError());
 }
 
 cudaError_t launch_predecessors(SpecId id, const uint64_t* xs, uint64_t n, uint64_t* out,
                                 uint8_t* count, cudaStream_t stream) {
+  LC_CUSTOM_OR(id)
+  if (id == SpecId::CUSTOM)
+    return jit_launch(custom->predecessors, grid_for(n, kThreads), kThreads, 0, stream, xs, n, out, count);
   LC_DISPATCH(id, predecessors_kernel<S><<<grid_for(n, kThreads), kThreads, 0, stream>>>(xs, n, out, count);
               return cudaGetLastError());
 }
@@ -703,6 +725,8 @@ cudaError_t launch_predecessors(SpecId id, const uint64_t* xs, uint64_t n, uint6
 cudaError_t launch_clock(SpecId id, const uint64_t* xs, uint64_t n, uint64_t t, uint64_t* out,
                          cudaStream_t stream) {
   const unsigned g = static_cast<unsigned>((n + 32u * 128u - 1) / (32u * 128u));
+  LC_CUSTOM_OR(id)
+  if (id == SpecId::CUSTOM) return jit_launch(custom->clock, g == 0 ? 1 : g, 128, 0, stream, xs, n, t, out);
   LC_DISPATCH(id, clock_kernel<S><<<g == 0 ? 1 : g, 128, 0, stream>>>(xs, n, t, out); return cudaGetLastError());
 }
 
@@ -712,6 +736,9 @@ cudaError_t launch_enumerate(SpecId id, uint32_t F, uint64_t r2_lo, uint64_t r2_
   const uint64_t units = rows * 8;  // A5/1: 2^19 virtual slots per row in units of 2^16 (minis: 1 per row)
   const unsigned grid = static_cast<unsigned>(units == 0 ? 1 : (units > (1u << 20) ? (1u << 20) : units));
   if (launches) *launches += 1;
+  LC_CUSTOM_OR(id)
+  if (id == SpecId::CUSTOM)
+    return jit_launch(custom->enumerate, grid, 256, 0, stream, r2_lo, r2_hi, F, out, cap, d_count);
   LC_DISPATCH(id, enumerate_plane_kernel<S><<<grid, 256, 0, stream>>>(r2_lo, r2_hi, F, out, cap, d_count);
               return cudaGetLastError());
 }
@@ -779,5 +806,7 @@ cudaError_t launch_first_missing(const uint64_t* set, uint64_t m, const uint64_t
   first_missing_kernel<<<grid_for(n, kThreads), kThreads, 0, stream>>>(set, m, q, n, first);
   return cudaGetLastError();
 }
+
+#endif  // !__CUDACC_RTC__
 
 }  // namespace lc

@@ -7,13 +7,18 @@
 // cipher.py:90-131 turned sideways.
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cstdint>
+#endif
 
 namespace lc {
 
 // Compile-time cipher instance (cipher.py:173-194).  Tap masks fit 32 bits (l <= 23).
+// WINDOW_: clocks after a special node before R3 can be back at F -- R3's period through
+// F (2^l3 - 1 for the built-ins' maximal-period registers; runtime-specialised custom
+// specs pass their own, see csrc/jit.cu).
 template <int L1_, int L2_, int L3_, uint32_t T1_, uint32_t T2_, uint32_t T3_, int C1_, int C2_,
-          int C3_, uint32_t DEFAULT_F_>
+          int C3_, uint32_t DEFAULT_F_, uint64_t WINDOW_ = (1ull << L3_) - 1>
 struct Spec {
   static constexpr int L1 = L1_, L2 = L2_, L3 = L3_;
   static constexpr int O2 = L1, O3 = L1 + L2, NB = L1 + L2 + L3;
@@ -21,7 +26,7 @@ struct Spec {
   static constexpr int CT1 = C1_, CT2 = C2_, CT3 = C3_;
   static constexpr uint32_t DEFAULT_F = DEFAULT_F_;  // default_fixed_r3 (cipher.py:405-417)
   static constexpr uint64_t M1 = (1ull << L1) - 1, M2 = (1ull << L2) - 1, M3 = (1ull << L3) - 1;
-  static constexpr uint64_t WINDOW = M3;  // R3 period: no candidate before 2^l3 - 1 clocks
+  static constexpr uint64_t WINDOW = WINDOW_;  // R3 period: no candidate before this many clocks
 };
 
 // A5/1: lengths (19,22,23), taps R1{13,16,17,18} R2{20,21} R3{7,20,21,22}, clock (8,10,10)
@@ -53,12 +58,14 @@ __device__ __forceinline__ uint32_t clock_enable(uint32_t ck, uint32_t ci, uint3
   return lop3<0xE7>(ck, ci, cj);
 }
 
+constexpr int popcount_ce(uint32_t v) { return v ? static_cast<int>(v & 1u) + popcount_ce(v >> 1) : 0; }
+
 // Bit 0 of a clocked register receives the XOR of its taps: r0' = e ? xor(taps) : r0.
 // Taps are folded three at a time; the last fold is fused with the insert when at
 // most one tap remains (2 taps: x = t0^t1^r0, r0' = r0 ^ (e & x) -- 2 LOP3).
 template <uint32_t TM, int L, int OFF, int NB>
 __device__ __forceinline__ uint32_t feedback_insert(const uint32_t (&s)[NB], uint32_t e) {
-  constexpr int n = __builtin_popcount(TM);
+  constexpr int n = popcount_ce(TM);
   uint32_t t[4] = {0, 0, 0, 0};
   int k = 0;
 #pragma unroll

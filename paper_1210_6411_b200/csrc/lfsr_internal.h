@@ -1,9 +1,11 @@
 // Host/device shared declarations for the lfsr_b200 kernels (not part of the C ABI).
 #pragma once
 
+#ifndef __CUDACC_RTC__  // (csrc/jit.cu compiles the kernels with NVRTC: device parts only)
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
+#endif
 
 // Bounds / invariant checks of the checked build (-DLC_CHECKS=1, __graft_entry__.build()
 // writes it to _lib/checked/; tests/test_gpu_checked.py runs every kernel mode on it): a
@@ -30,7 +32,9 @@
 
 namespace lc {
 
-enum class SpecId { A51 = 0, MINI567 = 1, MINI789 = 2, UNSUPPORTED = -1 };
+// CUSTOM: a valid cipher spec without a precompiled kernel; its kernels are compiled for
+// it at first use (csrc/jit.cu) and the calling thread's current custom spec selects them.
+enum class SpecId { A51 = 0, MINI567 = 1, MINI789 = 2, CUSTOM = 3, UNSUPPORTED = -1 };
 
 constexpr int kWalkThreads = 128;
 constexpr uint64_t kInf = ~0ull;
@@ -90,8 +94,10 @@ struct WalkParams {
   const unsigned long long* n_dev;  // resume round queued without a host sync: item count on the device (else null)
   uint64_t park_min;                // park only while the round has more than this many items
   uint64_t pool_cap;                // ResumeRec slots in `pool` (a warp that does not fit keeps walking)
+  uint64_t window;                  // R3's period through F (custom specs; built-ins use Spec::WINDOW)
 };
 
+#ifndef __CUDACC_RTC__
 // Launchers (defined in the .cu files); all enqueue on `stream`.
 // rearm: the variant that bounds each lane's next special node by R3's distance to F
 // (WalkParams::need3) instead of checking every step once armed.
@@ -224,5 +230,7 @@ cudaError_t sort_records_device(uint64_t n, uint64_t* const* cols, int ncols, vo
 
 cudaError_t launch_first_missing(const uint64_t* set, uint64_t m, const uint64_t* q, uint64_t n,
                                  unsigned long long* first, cudaStream_t stream);
+
+#endif  // !__CUDACC_RTC__
 
 }  // namespace lc

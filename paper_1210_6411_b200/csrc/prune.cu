@@ -22,11 +22,16 @@
 // newest pending entry.  Both paths end in one shared child computation (three register
 // unsteps, cipher.py:221-225, and a select), so a warp's lanes diverge only over a few
 // predicated instructions.
+#ifndef __CUDACC_RTC__
 #include <cstdint>
 #include <cstdlib>
+#endif
 
 #include "lfsr_common.cuh"
 #include "lfsr_internal.h"
+#ifndef __CUDACC_RTC__
+#include "jit.h"
+#endif
 
 namespace lc {
 namespace {
@@ -574,6 +579,7 @@ __global__ void __launch_bounds__(kThreads2, LC_PRUNE2_MINBLOCKS) prune2_kernel(
 #endif
 constexpr int kRing2 = LC_PRUNE2_RING;
 
+#ifndef __CUDACC_RTC__
 template <class S>
 int blocks2(bool dfs) {
   int b = 1;
@@ -582,16 +588,26 @@ int blocks2(bool dfs) {
   return b > 0 ? b : 1;
 }
 
+#endif
+
 }  // namespace
+
+#ifndef __CUDACC_RTC__
 
 int prune2_blocks_per_sm(SpecId id, int mode) {
   switch (id) {
     case SpecId::A51: return blocks2<A51>(mode == 0);
     case SpecId::MINI567: return blocks2<MINI567>(mode == 0);
     case SpecId::MINI789: return blocks2<MINI789>(mode == 0);
+    case SpecId::CUSTOM: {
+      const CustomKernels* c = current_custom();
+      return c ? jit_blocks_per_sm(mode == 0 ? c->prune_dfs : c->prune_bfs, kThreads2) : 1;
+    }
     default: return 1;
   }
 }
+
+int prune2_ring() { return kRing2; }
 
 uint64_t prune2_spill_bytes(int blocks, uint32_t cap) {
   return static_cast<uint64_t>(blocks) * kThreads2 * cap * (8 + 2) + 512;
@@ -614,10 +630,18 @@ cudaError_t launch_prune2(SpecId id, uint32_t F, int mode, uint64_t limit, const
     case SpecId::A51: LC_PRUNE2_LAUNCH(A51) break;
     case SpecId::MINI567: LC_PRUNE2_LAUNCH(MINI567) break;
     case SpecId::MINI789: LC_PRUNE2_LAUNCH(MINI789) break;
+    case SpecId::CUSTOM: {
+      const CustomKernels* c = current_custom();
+      if (!c) return cudaErrorInvalidValue;
+      return jit_launch(mode == 0 ? c->prune_dfs : c->prune_bfs, blocks, kThreads2, 0, stream, cands, n, F, limit,
+                        removed, work, queue, spill_node, spill_dm, spill_cap);
+    }
     default: return cudaErrorInvalidValue;
   }
 #undef LC_PRUNE2_LAUNCH
   return cudaGetLastError();
 }
+
+#endif  // !__CUDACC_RTC__
 
 }  // namespace lc

@@ -38,7 +38,10 @@ namespace {
 #endif
 
 constexpr uint32_t kFullMask = 0xffffffffu;
-constexpr int kSortThreads = 256;
+#ifndef LC_SORT_THREADS
+#define LC_SORT_THREADS 256
+#endif
+constexpr int kSortThreads = LC_SORT_THREADS;  // a multiple of 256 (threads 0..255 own a digit each)
 constexpr int kSortWarps = kSortThreads / 32;
 #ifndef LC_SORT_ITEMS
 #define LC_SORT_ITEMS 12
@@ -201,7 +204,7 @@ __global__ void __launch_bounds__(kSortThreads, LC_SORT_MINBLOCKS) sort_pass_ker
   unsigned long long* gbase = reinterpret_cast<unsigned long long*>(whist + kSortWarps * kWhistStride + 8);
   uint32_t* loff = reinterpret_cast<uint32_t*>(gbase + kBins);
   __shared__ unsigned int tile_s;
-  __shared__ uint32_t wsum[kSortWarps];
+  __shared__ uint32_t wsum[kBins / 32];
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid == 0) tile_s = atomicAdd(&ctl->tickets[byte], 1u);
@@ -247,44 +250,49 @@ __global__ void __launch_bounds__(kSortThreads, LC_SORT_MINBLOCKS) sort_pass_ker
   }
   __syncthreads();
 
-  // ---- digit d (thread d): warp prefixes, tile count, publish, tile-local offsets
+  // ---- digit d (thread d < 256): warp prefixes, tile count, publish, tile-local offsets
   const int d = tid;
-  uint32_t cnt = 0;
-#pragma unroll
-  for (int v = 0; v < kSortWarps; ++v) {
-    const uint32_t c = whist[v * kWhistStride + d];
-    whist[v * kWhistStride + d] = cnt;
-    cnt += c;
-  }
+  const bool owns_digit = tid < kBins;  // whole warps
+  uint32_t cnt = 0, incl = 0;
   const uint64_t epoch = static_cast<uint64_t>(byte + 1) << 40;
   volatile uint64_t* st = status;
-  if (tile == 0) st[d] = kFlagPrefix | epoch | cnt;
-  else st[tile * kBins + d] = kFlagAgg | epoch | cnt;
-  uint32_t incl = cnt;  // tile-local exclusive scan over the digits
+  if (owns_digit) {
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t v = __shfl_up_sync(kFullMask, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) wsum[w] = incl;
-  __syncthreads();
-  uint32_t wpre = 0;
-#pragma unroll
-  for (int v = 0; v < kSortWarps; ++v) wpre += v < w ? wsum[v] : 0u;
-  loff[d] = wpre + incl - cnt;
-  uint64_t excl = 0;  // decoupled look-back: this digit's offset among earlier tiles
-  if (tile > 0) {
-    for (int64_t p = static_cast<int64_t>(tile) - 1; p >= 0; --p) {
-      uint64_t s;
-      do {
-        s = st[p * kBins + d];
-      } while ((s & (0xffull << 40)) != epoch || (s & (3ull << 48)) == 0);
-      excl += s & kValueMask;
-      if (s & kFlagPrefix) break;
+    for (int v = 0; v < kSortWarps; ++v) {
+      const uint32_t c = whist[v * kWhistStride + d];
+      whist[v * kWhistStride + d] = cnt;
+      cnt += c;
     }
-    st[tile * kBins + d] = kFlagPrefix | epoch | (excl + cnt);
+    if (tile == 0) st[d] = kFlagPrefix | epoch | cnt;
+    else st[tile * kBins + d] = kFlagAgg | epoch | cnt;
+    incl = cnt;  // tile-local exclusive scan over the digits
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(kFullMask, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[w] = incl;
   }
-  gbase[d] = ctl->hist[byte][d] + excl;
+  __syncthreads();
+  if (owns_digit) {
+    uint32_t wpre = 0;
+#pragma unroll
+    for (int v = 0; v < kBins / 32; ++v) wpre += v < w ? wsum[v] : 0u;
+    loff[d] = wpre + incl - cnt;
+    uint64_t excl = 0;  // decoupled look-back: this digit's offset among earlier tiles
+    if (tile > 0) {
+      for (int64_t p = static_cast<int64_t>(tile) - 1; p >= 0; --p) {
+        uint64_t sv;
+        do {
+          sv = st[p * kBins + d];
+        } while ((sv & (0xffull << 40)) != epoch || (sv & (3ull << 48)) == 0);
+        excl += sv & kValueMask;
+        if (sv & kFlagPrefix) break;
+      }
+      st[tile * kBins + d] = kFlagPrefix | epoch | (excl + cnt);
+    }
+    gbase[d] = ctl->hist[byte][d] + excl;
+  }
   if (!first) cp_async_wait_all();
   __syncthreads();
 

@@ -22,12 +22,17 @@
 //    the input order regardless of scheduling;
 //  * the per-leg cap audit reproduces the reference's StrideError condition exactly
 //    (DESIGN.md "Cap").
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#endif
 
 #include "lfsr_common.cuh"
 #include "lfsr_internal.h"
+#ifndef __CUDACC_RTC__
+#include "jit.h"
+#endif
 
 namespace lc {
 
@@ -36,6 +41,14 @@ namespace {
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kChunk = 1u << 20;  // max steps between control points (abort polling)
 constexpr int kQueueStride = 16;       // u64 words between queue counters (128 B)
+
+// Clocks after a special node before R3 can be back at F: the spec's compile-time period
+// (2^l3 - 1 for the built-ins), or, for runtime-compiled custom specs (Spec WINDOW 0),
+// the period of R3's cycle through F computed on the host (WalkParams::window).
+template <class S>
+__device__ __forceinline__ uint64_t window_of(const WalkParams& p) {
+  return S::WINDOW ? S::WINDOW : p.window;
+}
 
 #ifndef LC_WALK_UNROLL
 #define LC_WALK_UNROLL 16  // steps per unchecked-loop iteration (same-box A/B: 16 > 4 > 8 by ~0.3 %)
@@ -229,7 +242,7 @@ __device__ __forceinline__ void whole_warp_refill(const WalkParams& p, volatile 
   // a start on the fixed plane whose R3 is clocked at once cannot meet R3 == F again
   // for 2^l3 - 1 clocks
   all_safe = __all_sync(kFull, all_safe);
-  const uint64_t first = max(p.stride, static_cast<uint64_t>(all_safe ? S::WINDOW : 1ull));
+  const uint64_t first = max(p.stride, static_cast<uint64_t>(all_safe ? window_of<S>(p) : 1ull));
   const uint64_t arm = sat_add(t, first), dead = sat_add(t, max(p.stride, p.cap1));
   __syncwarp();
   LaneMeta* const meta = p.meta + gtid * 32u;
@@ -315,7 +328,7 @@ __device__ __forceinline__ void lane_refill(const WalkParams& p, volatile WalkSh
       LaneMeta m;
       m.walk = k;
       m.leg_start = t;
-      m.arm_at = sat_add(t, max(p.stride, static_cast<uint64_t>(safe ? S::WINDOW : 1ull)));
+      m.arm_at = sat_add(t, max(p.stride, static_cast<uint64_t>(safe ? window_of<S>(p) : 1ull)));
       m.deadline = sat_add(t, max(p.stride, p.cap1));
       m.legs_done = 0u;
       m.pad = 0u;
@@ -434,7 +447,7 @@ __device__ __forceinline__ void handle_events(const WalkParams& p, volatile Walk
       } else {
         // the lane continues from the candidate it reached (bitslice.py:313-315)
         m.leg_start = t;
-        m.arm_at = sat_add(t, S::WINDOW);
+        m.arm_at = sat_add(t, window_of<S>(p));
         m.deadline = sat_add(t, p.cap1);
         m.pad = 0u;
       }
@@ -637,6 +650,7 @@ __global__ void mode_probe_kernel(const uint64_t* __restrict__ starts, uint64_t 
   if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) *mode = 0u;
 }
 
+#ifndef __CUDACC_RTC__  // host launchers (csrc/jit.cu compiles the device code alone)
 template <class S, bool SF>
 cudaError_t launch_t(const WalkParams& p, bool rearm, int blocks, cudaStream_t stream) {
   if (rearm) walk_kernel<S, SF, true><<<blocks, kWalkThreads, 0, stream>>>(p);
@@ -655,7 +669,11 @@ int occupancy_t() {
   return m > 0 ? m : 1;
 }
 
+#endif
+
 }  // namespace
+
+#ifndef __CUDACC_RTC__
 
 cudaError_t launch_init_stats(uint64_t* stats, uint64_t hist_lo, uint32_t hist_shift, uint32_t hist_bins,
                               unsigned long long* queues, uint32_t nq, unsigned int* exhausted,
@@ -683,6 +701,11 @@ cudaError_t launch_mode_probe(SpecId id, const uint64_t* starts, uint64_t n, uin
     case SpecId::A51: mode_probe_kernel<A51><<<g ? g : 1, 256, 0, stream>>>(starts, n, F, mode_word); break;
     case SpecId::MINI567: mode_probe_kernel<MINI567><<<g ? g : 1, 256, 0, stream>>>(starts, n, F, mode_word); break;
     case SpecId::MINI789: mode_probe_kernel<MINI789><<<g ? g : 1, 256, 0, stream>>>(starts, n, F, mode_word); break;
+    case SpecId::CUSTOM: {
+      const CustomKernels* c = current_custom();
+      if (!c) return cudaErrorInvalidValue;
+      return jit_launch(c->mode_probe, g ? g : 1, 256, 0, stream, starts, n, F, mode_word);
+    }
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -699,6 +722,11 @@ cudaError_t launch_walk(SpecId id, bool static_f, bool rearm, const WalkParams& 
     case SpecId::MINI789:
       return static_f ? launch_t<MINI789, true>(p, rearm, blocks, stream)
                       : launch_t<MINI789, false>(p, rearm, blocks, stream);
+    case SpecId::CUSTOM: {  // runtime-compiled for the spec, runtime F (csrc/jit.cu)
+      const CustomKernels* c = current_custom();
+      if (!c) return cudaErrorInvalidValue;
+      return jit_launch(rearm ? c->walk_rearm : c->walk_plain, blocks, kWalkThreads, 0, stream, p);
+    }
     default:
       return cudaErrorInvalidValue;
   }
@@ -709,8 +737,16 @@ int walk_blocks_per_sm(SpecId id, bool static_f) {
     case SpecId::A51: return static_f ? occupancy_t<A51, true>() : occupancy_t<A51, false>();
     case SpecId::MINI567: return static_f ? occupancy_t<MINI567, true>() : occupancy_t<MINI567, false>();
     case SpecId::MINI789: return static_f ? occupancy_t<MINI789, true>() : occupancy_t<MINI789, false>();
+    case SpecId::CUSTOM: {
+      const CustomKernels* c = current_custom();
+      if (!c) return 1;
+      const int a = jit_blocks_per_sm(c->walk_plain, kWalkThreads), b = jit_blocks_per_sm(c->walk_rearm, kWalkThreads);
+      return a < b ? a : b;
+    }
     default: return 1;
   }
 }
+
+#endif  // !__CUDACC_RTC__
 
 }  // namespace lc
