@@ -80,6 +80,10 @@ typedef struct lc_ctx lc_ctx;
 int lc_abi_version(void);
 const char *lc_last_error(void);
 int lc_device_count(int *count);
+/* Compile every kernel for a (custom) spec with NVRTC and discard the result: no device
+ * needed.  LC_ERR_UNSUPPORTED with the compiler log in lc_last_error() on failure.  (The
+ * kernels are compiled and loaded at the spec's first use anyway; this is the check.) */
+int lc_spec_compile_check(const lc_spec *spec);
 
 /* One context per (device, host thread).  Owns scratch buffers and a stream. */
 int lc_ctx_create(int device, lc_ctx **out);

@@ -50,6 +50,7 @@ _SIGNATURES = {
     "lc_abi_version": ([], C.c_int),
     "lc_last_error": ([], C.c_char_p),
     "lc_device_count": ([C.POINTER(C.c_int)], C.c_int),
+    "lc_spec_compile_check": ([C.POINTER(lc_spec)], C.c_int),
     "lc_ctx_create": ([C.c_int, C.POINTER(C.c_void_p)], C.c_int),
     "lc_ctx_destroy": ([_vp], C.c_int),
     "lc_ctx_sm_count": ([_vp, C.POINTER(C.c_int)], C.c_int),

@@ -53,7 +53,10 @@ Nvrtc& nvrtc(std::string* err) {
   static Nvrtc n;
   static std::once_flag once;
   std::call_once(once, [] {
-    for (const char* lib : {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so"})
+    // the toolkit's own NVRTC first: a bare soname can resolve to an older copy another
+    // library of the process (torch) already loaded
+    for (const char* lib : {"/usr/local/cuda/lib64/libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so",
+                            "libnvrtc.so.12", "libnvrtc.so"})
       if ((n.h = dlopen(lib, RTLD_NOW | RTLD_LOCAL)) != nullptr) break;
     if (!n.h) return;
     n.ok = sym(n.h, "nvrtcCreateProgram", n.create) && sym(n.h, "nvrtcAddNameExpression", n.add_name) &&
@@ -130,6 +133,7 @@ bool compile_file(const std::string& dir, const char* file, const std::vector<st
     lowered->push_back(l ? l : "");
   }
   nv.destroy(&prog);
+  if (!lib) return true;  // compile-only check
   const cudaError_t e = cudaLibraryLoadData(lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
   if (e != cudaSuccess) {
     *err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e);
@@ -141,6 +145,7 @@ bool compile_file(const std::string& dir, const char* file, const std::vector<st
 std::mutex g_mu;
 std::map<std::string, std::unique_ptr<CustomKernels>> g_cache;
 thread_local const CustomKernels* tl_current = nullptr;
+CustomKernels g_compile_ok;  // build_custom's result for a successful compile-only check
 
 }  // namespace
 
@@ -170,7 +175,17 @@ int custom_spec_error(const lc_spec* s, std::string* err) {
   return 0;
 }
 
-const CustomKernels* custom_kernels_for(const lc_spec* s, std::string* err) {
+namespace {
+const CustomKernels* build_custom(const lc_spec* s, bool load, std::string* err);
+}
+
+const CustomKernels* custom_kernels_for(const lc_spec* s, std::string* err) { return build_custom(s, true, err); }
+
+int custom_compile_check(const lc_spec* s, std::string* err) { return build_custom(s, false, err) ? 0 : 1; }
+
+namespace {
+// load = false: compile every unit (NVRTC only, no device), return &dummy on success
+const CustomKernels* build_custom(const lc_spec* s, bool load, std::string* err) {
   if (custom_spec_error(s, err)) return nullptr;
   char key[256];
   snprintf(key, sizeof key, "%d,%d,%d,%llu,%llu,%llu,%d,%d,%d", s->lengths[0], s->lengths[1], s->lengths[2],
@@ -178,7 +193,7 @@ const CustomKernels* custom_kernels_for(const lc_spec* s, std::string* err) {
            static_cast<unsigned long long>(s->tap_masks[2]), s->clock_taps[0], s->clock_taps[1], s->clock_taps[2]);
   std::lock_guard<std::mutex> lock(g_mu);
   auto it = g_cache.find(key);
-  if (it != g_cache.end()) return it->second.get();
+  if (load && it != g_cache.end()) return it->second.get();
   const std::string dir = csrc_dir();
   if (dir.empty()) {
     *err = "kernel sources (csrc/) not found next to the library";
@@ -202,8 +217,9 @@ const CustomKernels* custom_kernels_for(const lc_spec* s, std::string* err) {
     std::vector<std::string> names;
     std::vector<cudaKernel_t*> out;
   };
-  char ring[16];
+  char ring[16], stack3[16];
   snprintf(ring, sizeof ring, "%d", prune2_ring());
+  snprintf(stack3, sizeof stack3, "%d", prune3_stack());
   Unit units[] = {
       {"walk.cu",
        {"&lc::walk_kernel<" + S + ", false, false>", "&lc::walk_kernel<" + S + ", false, true>",
@@ -214,13 +230,15 @@ const CustomKernels* custom_kernels_for(const lc_spec* s, std::string* err) {
         "&lc::enumerate_plane_kernel<" + S + ">"},
        {&k->is_candidate, &k->predecessors, &k->clock, &k->enumerate}},
       {"prune.cu",
-       {"&lc::prune2_kernel<" + S + ", " + ring + ", true>", "&lc::prune2_kernel<" + S + ", " + ring + ", false>"},
-       {&k->prune_dfs, &k->prune_bfs}},
+       {"&lc::prune2_kernel<" + S + ", " + ring + ", true>", "&lc::prune2_kernel<" + S + ", " + ring + ", false>",
+        "&lc::prune3_kernel<" + S + ", " + stack3 + ">"},
+       {&k->prune_dfs, &k->prune_bfs, &k->prune3_dfs}},
   };
   for (Unit& u : units) {
     cudaLibrary_t lib;
     std::vector<std::string> lowered;
-    if (!compile_file(dir, u.file, u.names, &lib, &lowered, err)) return nullptr;
+    if (!compile_file(dir, u.file, u.names, load ? &lib : nullptr, &lowered, err)) return nullptr;
+    if (!load) continue;
     for (size_t i = 0; i < u.names.size(); ++i) {
       const cudaError_t e = cudaLibraryGetKernel(u.out[i], lib, lowered[i].c_str());
       if (e != cudaSuccess) {
@@ -229,10 +247,12 @@ const CustomKernels* custom_kernels_for(const lc_spec* s, std::string* err) {
       }
     }
   }
+  if (!load) return &g_compile_ok;
   const CustomKernels* p = k.get();
   g_cache.emplace(key, std::move(k));
   return p;
 }
+}  // namespace
 
 void set_current_custom(const CustomKernels* k) { tl_current = k; }
 const CustomKernels* current_custom() { return tl_current; }

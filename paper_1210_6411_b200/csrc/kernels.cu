@@ -362,9 +362,16 @@ __global__ void __launch_bounds__(256) enumerate_plane_kernel(uint64_t r2_lo, ui
         const uint64_t slot = g0 + vbase + 128 * u + 4 * lane;  // 32-byte aligned
         if (k < nquads) {
           if (slot + 3 < cap) {
+#if __CUDACC_VER_MAJOR__ > 12 || (__CUDACC_VER_MAJOR__ == 12 && __CUDACC_VER_MINOR__ >= 9)
             asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(out + slot), "l"(val[u][0]),
                          "l"(val[u][1]), "l"(val[u][2]), "l"(val[u][3])
                          : "memory");
+#else  // 256-bit stores need PTX ISA 8.8 (a runtime compiler older than CUDA 12.9): two 128-bit
+            asm volatile("st.global.v2.b64 [%0], {%1, %2};" ::"l"(out + slot), "l"(val[u][0]), "l"(val[u][1])
+                         : "memory");
+            asm volatile("st.global.v2.b64 [%0], {%1, %2};" ::"l"(out + slot + 2), "l"(val[u][2]), "l"(val[u][3])
+                         : "memory");
+#endif
           } else {
 #pragma unroll
             for (int e = 0; e < 4; ++e)

@@ -66,19 +66,28 @@ constexpr int popcount_ce(uint32_t v) { return v ? static_cast<int>(v & 1u) + po
 template <uint32_t TM, int L, int OFF, int NB>
 __device__ __forceinline__ uint32_t feedback_insert(const uint32_t (&s)[NB], uint32_t e) {
   constexpr int n = popcount_ce(TM);
-  uint32_t t[4] = {0, 0, 0, 0};
+  static_assert(n >= 1 && n <= 32, "tap count");
+  uint32_t t[n > 4 ? n : 4] = {};
   int k = 0;
 #pragma unroll
   for (int i = 0; i < L; ++i)
-    if ((TM >> i) & 1u) t[k++ & 3] = s[OFF + i];
+    if ((TM >> i) & 1u) t[k++] = s[OFF + i];
   const uint32_t r0 = s[OFF];
-  if constexpr (n == 2) {
+  if constexpr (n == 1) {
+    return mux(e, t[0], r0);
+  } else if constexpr (n == 2) {
     return lop3<0x78>(r0, e, xor3(t[0], t[1], r0));  // r0 ^ (e & (t0 ^ t1 ^ r0))
   } else if constexpr (n == 3) {
     return mux(e, xor3(t[0], t[1], t[2]), r0);
-  } else {
-    static_assert(n == 4, "tap count");
+  } else if constexpr (n == 4) {
     return mux(e, lop3<0x3C>(xor3(t[0], t[1], t[2]), t[3], 0u), r0);  // 0x3C: a ^ b
+  } else {  // custom specs with more taps: fold two more per LOP3
+    uint32_t x = xor3(t[0], t[1], t[2]);
+    int j = 3;
+#pragma unroll
+    for (; j + 1 < n; j += 2) x = xor3(x, t[j], t[j + 1]);
+    if (j < n) x = lop3<0x3C>(x, t[j], 0u);
+    return mux(e, x, r0);
   }
 }
 

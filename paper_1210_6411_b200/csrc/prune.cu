@@ -574,6 +574,206 @@ __global__ void __launch_bounds__(kThreads2, LC_PRUNE2_MINBLOCKS) prune2_kernel(
 #endif
 }
 
+// ---------------------------------------------------------------------------- K3 v3
+//
+// DFS mode with one uniform step per expansion.  The pending branch points are a plain
+// per-lane stack of (node, depth, remaining children) entries; every step a lane
+// expands its current node and moves to the next node of the reference's preorder:
+//   * the node has children: its highest child; the rest go on the stack as one entry
+//     (a push), unless it was the only one;
+//   * a leaf: the highest remaining child of the stack's top entry (a load); the top
+//     entry keeps the others (a store of its new mask) or is popped.
+// Both cases are the same instructions on a selected source entry: one predicated
+// 16-byte shared-memory load, one predicated store, three register unsteps and a
+// select -- no per-lane branches besides the rare ones (a special-node child, the depth
+// abort, a traversal's end).
+//
+// Stack entries are ancestors of the current node at distinct depths, so a traversal
+// that aborts at depth `limit` never holds more than `limit` of them (launched for
+// limit <= kSpill3Max).  Deep segments keep hundreds pending (the time-weighted median
+// stack height of the A5/1 slice is ~250), so the stack lives in global memory -- the
+// lane's own array, written through on every push and mask update -- and the newest
+// K entries are cached in a shared-memory ring ([slot][thread], 16 B per entry,
+// conflict-free), which is what the step reads.  The ring is kept stocked ahead of
+// the pops: once fewer than kLow3 entries are cached, the kChunk3 entries below are
+// requested with cp.async (no register staging, no stall), so a pop finds its entry
+// already in shared memory; a full ring just forgets its oldest kChunk3 (they are in
+// global memory already).
+constexpr int kThreads3 = 128;
+#ifndef LC_PRUNE3_STACK
+#define LC_PRUNE3_STACK 16
+#endif
+#ifndef LC_PRUNE3_CHUNK
+#define LC_PRUNE3_CHUNK 4
+#endif
+#ifndef LC_PRUNE3_LOW
+#define LC_PRUNE3_LOW 4
+#endif
+#ifndef LC_PRUNE3_BURST
+#define LC_PRUNE3_BURST 4
+#endif
+constexpr int kStack3 = LC_PRUNE3_STACK;
+constexpr int kChunk3 = LC_PRUNE3_CHUNK;  // entries per prefetch / per eviction
+constexpr int kLow3 = LC_PRUNE3_LOW;      // prefetch below this many cached entries
+constexpr int kBurst3 = LC_PRUNE3_BURST;  // steps between warp votes for new candidates
+static_assert((kStack3 & (kStack3 - 1)) == 0, "stack ring is a power of two");
+static_assert(kChunk3 >= 1 && kLow3 + kChunk3 <= kStack3, "a prefetch fits the ring");
+constexpr uint32_t kSpill3Max = 4096;
+constexpr int kStack3Bytes = kStack3 * kThreads3 * 16;
+
+// child set with the special-node test behind a cheap necessary condition: unstep(R3)
+// == F needs R3 >> 1 == F's low bits
+template <class S>
+__device__ __forceinline__ uint32_t child_set3(const uint8_t* tbl, uint32_t r1, uint32_t r2, uint32_t r3,
+                                               uint32_t F) {
+  constexpr uint32_t LOW = static_cast<uint32_t>(S::M3 >> 1);
+  uint32_t m = tbl[pair_index<S>(r1, r2, r3)];
+  if ((r3 >> 1) == (F & LOW)) {
+    if (unstep2<S::L3, S::T3>(r3) == F) {
+#pragma unroll
+      for (uint32_t q = 1; q < 4; ++q) {
+        uint32_t c1 = r1, c2 = r2, c3 = r3;
+        child2<S>(c1, c2, c3, q);
+        if (((m >> q) & 1u) && tbl[pair_index<S>(c1, c2, c3)] != 0u) m &= ~(1u << q);
+      }
+    }
+  }
+  return m;
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t smem, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <class S, int K>
+__global__ void __launch_bounds__(kThreads3) prune3_kernel(const uint64_t* __restrict__ cands, uint64_t n,
+                                                           uint32_t F, uint32_t limit,
+                                                           uint8_t* __restrict__ removed,
+                                                           uint64_t* __restrict__ work, unsigned long long* queue,
+                                                           uint4* gstack, uint32_t gcap) {
+  extern __shared__ uint4 ring[];  // [K][kThreads3] (dynamic: kStack3Bytes)
+  __shared__ uint8_t tbl[64];
+  if (threadIdx.x < 16) reinterpret_cast<uint32_t*>(tbl)[threadIdx.x] = kChildTable.w[threadIdx.x];
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t gtid = blockIdx.x * static_cast<uint64_t>(kThreads3) + threadIdx.x;
+  uint4* my = gstack + gtid * gcap;  // this lane's stack, logical index = position
+  uint4* my_ring = ring + threadIdx.x;
+  const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(my_ring));
+  constexpr uint32_t kSlot = kThreads3 * 16;  // bytes between a lane's ring slots
+  uint64_t i = 0, acc = 0;
+  uint32_t r1 = 0, r2 = 0, r3 = 0, d = 0;
+  uint32_t sp = 0;    // stack height: logical entries [0, sp), all in global memory
+  uint32_t lo = 0;    // the ring caches [lo, sp) (sp - lo <= K)
+  uint32_t pfhi = 0;  // entries [.., pfhi) may still be in flight from a prefetch (0: none)
+  bool have = false, drained = false;
+  for (;;) {
+    const uint32_t need = __ballot_sync(kFull, !have);
+    if (need != 0u) {
+      if (drained) {
+        if (need == kFull) break;
+      } else {
+        const int leader = __ffs(need) - 1;
+        unsigned long long base = 0;
+        if (static_cast<int>(lane) == leader) base = atomicAdd(queue, static_cast<unsigned long long>(__popc(need)));
+        base = __shfl_sync(kFull, base, leader);
+        if (base + __popc(need) >= n) drained = true;
+        if (!have) {
+          i = base + __popc(need & ((1u << lane) - 1u));
+          if (i < n) {
+            unpack2<S>(cands[i], r1, r2, r3);
+            d = 0;
+            acc = 0;
+            sp = lo = 0;
+            have = true;
+          }
+        }
+      }
+    }
+#pragma unroll 1
+    for (int k = 0; k < kBurst3; ++k) {
+      if (!have) break;
+      const uint32_t m = child_set3<S>(tbl, r1, r2, r3, F);
+      const bool leaf = m == 0u;
+      int fin = 0;  // 1 removed (traversal complete), 2 survivor (a child below the limit)
+      if (!leaf && d >= limit) {  // pipeline.py:138-141: the first child counts, then abort
+        acc += 1;
+        fin = 2;
+      } else if (leaf && sp == 0u) {
+        fin = 1;
+      }
+      if (fin != 0) {
+        LC_CHECK(i < n);
+        removed[i] = fin == 1 ? 1 : 0;
+        work[i] = acc;
+        have = false;
+        if (pfhi) cp_async_wait_all();  // nothing in flight into the ring across traversals
+        pfhi = 0;
+        break;
+      }
+      acc += __popc(m);
+      if (leaf) {
+        if (sp - 1u < pfhi) {  // the top entry may still be arriving
+          cp_async_wait_all();
+          pfhi = 0;
+        }
+        if (sp == lo) {  // not cached (no room was left to prefetch it): fetch it now
+          LC_CHECK(sp - 1u < gcap);
+          ring[((sp - 1u) & (K - 1)) * kThreads3 + threadIdx.x] = my[sp - 1u];
+          --lo;
+        }
+      }
+      const uint32_t top = (sp - 1u) & (K - 1);
+      uint4 e = make_uint4(r1, r2, r3, (d << 4) | m);
+      if (leaf) e = my_ring[top * kThreads3];
+      const uint32_t mask = e.w & 15u;
+      const uint32_t q = 31 - __clz(mask);  // the LIFO stack pops the last-pushed (highest) child first
+      const uint32_t rest = mask & ~(1u << q);
+      const uint32_t ed = e.w >> 4;
+      const uint32_t w = (ed << 4) | rest;
+      if (rest != 0u) {
+        if (leaf) {  // the top entry keeps its other children
+          my_ring[top * kThreads3].w = w;
+          my[sp - 1u].w = w;
+        } else {  // push (the ring forgets its oldest chunk when full: they are in memory)
+          if (sp - lo == static_cast<uint32_t>(K)) {
+            if (pfhi) {
+              cp_async_wait_all();
+              pfhi = 0;
+            }
+            lo += kChunk3;
+          }
+          LC_CHECK(sp < gcap);
+          const uint4 ne = make_uint4(e.x, e.y, e.z, w);
+          my_ring[(sp & (K - 1)) * kThreads3] = ne;
+          my[sp] = ne;
+          ++sp;
+        }
+      } else if (leaf) {
+        --sp;
+      }
+      // keep the ring stocked ahead of the pops
+      if (lo != 0u && sp - lo < static_cast<uint32_t>(kLow3)) {
+        if (pfhi) cp_async_wait_all();
+        const uint32_t nb = lo < static_cast<uint32_t>(kChunk3) ? lo : static_cast<uint32_t>(kChunk3);
+        pfhi = lo;
+#pragma unroll
+        for (int j = 1; j <= kChunk3; ++j)
+          if (static_cast<uint32_t>(j) <= nb) cp_async16(ring_s + ((lo - j) & (K - 1)) * kSlot, my + (lo - j));
+        cp_async_commit();
+        lo -= nb;
+      }
+      r1 = e.x;
+      r2 = e.y;
+      r3 = e.z;
+      d = ed + 1;
+      child2<S>(r1, r2, r3, q);
+    }
+  }
+}
+
 #ifndef LC_PRUNE2_RING
 #define LC_PRUNE2_RING 16
 #endif
@@ -585,6 +785,21 @@ int blocks2(bool dfs) {
   int b = 1;
   if (dfs) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, prune2_kernel<S, kRing2, true>, kThreads2, 0);
   else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, prune2_kernel<S, kRing2, false>, kThreads2, 0);
+  return b > 0 ? b : 1;
+}
+
+template <class S>
+const void* kernel3() {
+  // (per call: the attribute is per device, and setting it is a cheap host call)
+  const void* k = reinterpret_cast<const void*>(prune3_kernel<S, kStack3>);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kStack3Bytes);
+  return k;
+}
+
+template <class S>
+int blocks3() {
+  int b = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel3<S>(), kThreads3, kStack3Bytes);
   return b > 0 ? b : 1;
 }
 
@@ -608,6 +823,53 @@ int prune2_blocks_per_sm(SpecId id, int mode) {
 }
 
 int prune2_ring() { return kRing2; }
+int prune3_stack() { return kStack3; }
+
+int prune3_blocks_per_sm(SpecId id) {
+  switch (id) {
+    case SpecId::A51: return blocks3<A51>();
+    case SpecId::MINI567: return blocks3<MINI567>();
+    case SpecId::MINI789: return blocks3<MINI789>();
+    case SpecId::CUSTOM: {
+      const CustomKernels* c = current_custom();
+      if (!c) return 1;
+      cudaFuncSetAttribute(reinterpret_cast<const void*>(c->prune3_dfs), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kStack3Bytes);
+      return jit_blocks_per_sm(c->prune3_dfs, kThreads3, kStack3Bytes);
+    }
+    default: return 1;
+  }
+}
+
+uint32_t prune3_max_limit() { return kSpill3Max; }
+int prune3_threads() { return kThreads3; }
+
+uint64_t prune3_spill_bytes(int blocks, uint32_t limit) {
+  return static_cast<uint64_t>(blocks) * kThreads3 * limit * sizeof(uint4);
+}
+
+cudaError_t launch_prune3(SpecId id, uint32_t F, uint32_t limit, const uint64_t* cands, uint64_t n,
+                          uint8_t* removed, uint64_t* work, unsigned long long* queue, void* spill, int blocks,
+                          cudaStream_t stream) {
+  uint4* sp = static_cast<uint4*>(spill);
+  const void* k = nullptr;
+  switch (id) {
+    case SpecId::A51: k = kernel3<A51>(); break;
+    case SpecId::MINI567: k = kernel3<MINI567>(); break;
+    case SpecId::MINI789: k = kernel3<MINI789>(); break;
+    case SpecId::CUSTOM: {
+      const CustomKernels* c = current_custom();
+      if (!c) return cudaErrorInvalidValue;
+      k = reinterpret_cast<const void*>(c->prune3_dfs);
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kStack3Bytes);
+      break;
+    }
+    default: return cudaErrorInvalidValue;
+  }
+  uint32_t cap = limit;
+  void* args[] = {&cands, &n, &F, &limit, &removed, &work, &queue, &sp, &cap};
+  return cudaLaunchKernel(k, blocks, kThreads3, args, kStack3Bytes, stream);
+}
 
 uint64_t prune2_spill_bytes(int blocks, uint32_t cap) {
   return static_cast<uint64_t>(blocks) * kThreads2 * cap * (8 + 2) + 512;

@@ -14,6 +14,7 @@ pytestmark = pytest.mark.gpu
 
 ODD = ("odd", (5, 7, 7), ((1, 4), (5, 6), (5, 6)), (2, 2, 3))
 ROT = ("rot", (6, 7, 7), ((2, 5), (3, 6), (6,)), (2, 3, 3))
+MANY = ("many_taps", (7, 8, 9), ((1, 2, 3, 4, 6), (0, 3, 4, 5, 6, 7), (3, 8)), (3, 3, 4))  # 5- and 6-tap folds
 
 
 def _spec(lc, d):
@@ -26,7 +27,7 @@ def _random_valid(spec, n, seed):
     return regs[0] | (regs[1] << np.uint64(spec.offsets[1])) | (regs[2] << np.uint64(spec.offsets[2]))
 
 
-@pytest.mark.parametrize("d", [ODD, ROT], ids=lambda d: d[0])
+@pytest.mark.parametrize("d", [ODD, ROT, MANY], ids=lambda d: d[0])
 def test_custom_spec_matches_restatement(gpu, lc, d):
     from oracle import port
     from paper_1210_6411_b200 import _batch
