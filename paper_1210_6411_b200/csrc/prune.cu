@@ -598,10 +598,16 @@ __global__ void __launch_bounds__(kThreads2, LC_PRUNE2_MINBLOCKS) prune2_kernel(
 // the pops: once fewer than kLow3 entries are cached, the kChunk3 entries below are
 // requested with cp.async (no register staging, no stall), so a pop finds its entry
 // already in shared memory; a full ring just forgets its oldest kChunk3 (they are in
-// global memory already).
+// global memory already).  The cached range always starts at a multiple of kChunk3, so
+// a refill is kChunk3 fixed-offset copies into consecutive slots.
+//
+// Divergence is what this kernel's speed is about (ncu at 2^26: 58 % of the lanes of
+// an issued warp instruction active with separate push / rewrite paths and variable
+// refills); the unified store and the aligned refills were worth 1.55x over K3 v2 at
+// 2^28 candidates (profiles/r02_prune3_ab.txt).
 constexpr int kThreads3 = 128;
 #ifndef LC_PRUNE3_STACK
-#define LC_PRUNE3_STACK 16
+#define LC_PRUNE3_STACK 8
 #endif
 #ifndef LC_PRUNE3_CHUNK
 #define LC_PRUNE3_CHUNK 4
@@ -610,7 +616,7 @@ constexpr int kThreads3 = 128;
 #define LC_PRUNE3_LOW 4
 #endif
 #ifndef LC_PRUNE3_BURST
-#define LC_PRUNE3_BURST 4
+#define LC_PRUNE3_BURST 8
 #endif
 constexpr int kStack3 = LC_PRUNE3_STACK;
 constexpr int kChunk3 = LC_PRUNE3_CHUNK;  // entries per prefetch / per eviction
@@ -620,6 +626,7 @@ static_assert((kStack3 & (kStack3 - 1)) == 0, "stack ring is a power of two");
 static_assert(kChunk3 >= 1 && kLow3 + kChunk3 <= kStack3, "a prefetch fits the ring");
 constexpr uint32_t kSpill3Max = 4096;
 constexpr int kStack3Bytes = kStack3 * kThreads3 * 16;
+static_assert(kStack3 % kChunk3 == 0, "aligned chunks tile the ring");
 
 // child set with the special-node test behind a cheap necessary condition: unstep(R3)
 // == F needs R3 >> 1 == F's low bits
@@ -720,9 +727,13 @@ __global__ void __launch_bounds__(kThreads3) prune3_kernel(const uint64_t* __res
           pfhi = 0;
         }
         if (sp == lo) {  // not cached (no room was left to prefetch it): fetch it now
-          LC_CHECK(sp - 1u < gcap);
-          ring[((sp - 1u) & (K - 1)) * kThreads3 + threadIdx.x] = my[sp - 1u];
-          --lo;
+          lo -= kChunk3;  // lo stays a multiple of the chunk: its slots are consecutive
+          const uint32_t s0 = ring_s + (lo & (K - 1)) * kSlot;
+#pragma unroll
+          for (int j = 0; j < kChunk3; ++j) cp_async16(s0 + j * kSlot, my + lo + j);
+          cp_async_commit();
+          cp_async_wait_all();
+          pfhi = 0;
         }
       }
       const uint32_t top = (sp - 1u) & (K - 1);
@@ -732,38 +743,32 @@ __global__ void __launch_bounds__(kThreads3) prune3_kernel(const uint64_t* __res
       const uint32_t q = 31 - __clz(mask);  // the LIFO stack pops the last-pushed (highest) child first
       const uint32_t rest = mask & ~(1u << q);
       const uint32_t ed = e.w >> 4;
-      const uint32_t w = (ed << 4) | rest;
+      // the entry keeping the other children: the top one rewritten (leaf) or a new one
+      // pushed -- one predicated 16-byte store to the ring and one to memory either way
+      const uint32_t idx = leaf ? sp - 1u : sp;
       if (rest != 0u) {
-        if (leaf) {  // the top entry keeps its other children
-          my_ring[top * kThreads3].w = w;
-          my[sp - 1u].w = w;
-        } else {  // push (the ring forgets its oldest chunk when full: they are in memory)
-          if (sp - lo == static_cast<uint32_t>(K)) {
-            if (pfhi) {
-              cp_async_wait_all();
-              pfhi = 0;
-            }
-            lo += kChunk3;
+        if (!leaf && sp - lo == static_cast<uint32_t>(K)) {  // ring full: forget its oldest chunk
+          if (pfhi) {
+            cp_async_wait_all();
+            pfhi = 0;
           }
-          LC_CHECK(sp < gcap);
-          const uint4 ne = make_uint4(e.x, e.y, e.z, w);
-          my_ring[(sp & (K - 1)) * kThreads3] = ne;
-          my[sp] = ne;
-          ++sp;
+          lo += kChunk3;
         }
-      } else if (leaf) {
-        --sp;
+        LC_CHECK(idx < gcap);
+        const uint4 ne = make_uint4(e.x, e.y, e.z, (ed << 4) | rest);
+        my_ring[(idx & (K - 1)) * kThreads3] = ne;
+        my[idx] = ne;
       }
+      sp = idx + (rest != 0u ? 1u : 0u);
       // keep the ring stocked ahead of the pops
       if (lo != 0u && sp - lo < static_cast<uint32_t>(kLow3)) {
         if (pfhi) cp_async_wait_all();
-        const uint32_t nb = lo < static_cast<uint32_t>(kChunk3) ? lo : static_cast<uint32_t>(kChunk3);
         pfhi = lo;
+        lo -= kChunk3;
+        const uint32_t s0 = ring_s + (lo & (K - 1)) * kSlot;
 #pragma unroll
-        for (int j = 1; j <= kChunk3; ++j)
-          if (static_cast<uint32_t>(j) <= nb) cp_async16(ring_s + ((lo - j) & (K - 1)) * kSlot, my + (lo - j));
+        for (int j = 0; j < kChunk3; ++j) cp_async16(s0 + j * kSlot, my + lo + j);
         cp_async_commit();
-        lo -= nb;
       }
       r1 = e.x;
       r2 = e.y;

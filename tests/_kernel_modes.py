@@ -5,7 +5,7 @@ mode also checks its results against the C restatement, so a run that finishes i
 correct run.
 
     LFSR_LIB=.../checked/liblfsr_b200.so python tests/_kernel_modes.py MODE
-    MODE: walk_warp | walk_lane | walk_park | walk_park_device | prune | prune_spill | enumerate | sort
+    MODE: walk_warp | walk_lane | walk_park | walk_park_device | prune | prune_v2 | prune_spill | enumerate | sort
 """
 
 from __future__ import annotations
@@ -67,7 +67,7 @@ def main(mode: str) -> None:
                                          C.c_void_p(stats.data_ptr()), C.c_void_p(st.cuda_stream)))
             torch.cuda.synchronize()
             assert (dst.cpu().numpy().view(np.uint64) == want.dst.reshape(-1)).all()
-    elif mode in ("prune", "prune_spill"):  # K3, dfs and bfs; prune_spill: tiny ring spill
+    elif mode in ("prune", "prune_v2", "prune_spill"):  # K3, dfs and bfs; prune_spill: tiny ring spill
         cands = lc.enumerate_candidates_array(lc.MINI789, m789)
         for how, limit in (("dfs", 40), ("dfs", 400), ("bfs", 300)):
             rem, work = _prune(lc, cands, how, limit, m789)

@@ -19,7 +19,8 @@ pytestmark = pytest.mark.gpu
 
 TARGET = os.path.join(ROOT, "tests", "_kernel_modes.py")
 CHECKED = os.path.join(ROOT, "paper_1210_6411_b200", "_lib", "checked", "liblfsr_b200.so")
-MODES = ["walk_warp", "walk_lane", "walk_park", "walk_park_device", "prune", "prune_spill", "enumerate", "sort"]
+MODES = ["walk_warp", "walk_lane", "walk_park", "walk_park_device", "prune", "prune_v2", "prune_spill", "enumerate",
+         "sort"]
 
 
 @pytest.mark.parametrize("mode", MODES)
@@ -27,7 +28,10 @@ def test_checked_build_runs_clean(gpu, mode):
     assert os.path.exists(CHECKED), "checked build missing: run __graft_entry__.build()"
     env = dict(os.environ, LFSR_LIB=CHECKED)
     if mode == "prune_spill":
-        env["LFSR_PRUNE_SPILL"] = "2"  # overflow the spill ring: exercises drop-and-climb
+        env["LFSR_PRUNE_SPILL"] = "2"  # v2's spill ring overflowed: exercises drop-and-climb
+        env["LFSR_PRUNE_V1"] = "2"
+    if mode == "prune_v2":  # DFS on the v2 kernel (the default DFS kernel is v3)
+        env["LFSR_PRUNE_V1"] = "2"
     out = subprocess.run([sys.executable, TARGET, mode], env=env, cwd=ROOT, capture_output=True, text=True,
                          timeout=900)
     log = out.stdout + out.stderr
