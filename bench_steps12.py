@@ -27,8 +27,41 @@ sys.path.insert(0, ROOT)
 R2_0 = 0x2AAA  # first R2 row of the slice
 
 
-def measure(ctx, stream, *, rows_log2: int = 13, prune_log2: int = 24, depth: int = 3000, walk_log2: int = 14,
-            cpu_sample: int = 1 << 14, keep=None) -> dict:
+def k3_roofline(expansions_per_s: float, lop3_peak: float, sm_mhz: float) -> dict:
+    """K3 is bound by instruction issue on the integer ALU pipe (no tensor or HBM work:
+    its stack traffic stays mostly in L2).  achieved = the live expansions/s times the
+    ALU-pipe warp instructions per expansion that ncu counted for this kernel
+    (profiles/r02_prune3_metrics.json); peak = the ALU pipe's warp-instruction rate,
+    i.e. the LOP3 issue peak measured in this process (lc_lop3_peak: one 32-lane ALU
+    instruction per 2 cycles per SM sub-partition) / 32 -- so frac is the ALU pipe's
+    busy fraction.  simt_efficiency says how much of that issue carries live lanes."""
+    path = os.path.join(ROOT, "profiles", "r02_prune3_metrics.json")
+    try:
+        with open(path) as f:
+            met = json.load(f)
+    except OSError:
+        return {"bound": "issue (integer ALU pipe)", "achieved": None, "peak": None, "frac": None,
+                "note": "profiles/r02_prune3_metrics.json missing"}
+    alu = float(met["alu_warp_inst_per_expansion"])
+    achieved = expansions_per_s * alu
+    peak = lop3_peak / 32.0
+    return {"bound": "issue (integer ALU pipe)", "achieved": achieved / 1e9, "peak": peak / 1e9,
+            "unit": "G ALU warp-instructions/s", "frac": achieved / peak,
+            "peak_source": f"lc_lop3_peak measured in this run / 32 lanes ({sm_mhz:.0f} MHz)",
+            "alu_warp_inst_per_expansion": alu,
+            "simt_efficiency": met["simt_efficiency"], "warp_inst_per_expansion": met["warp_inst_per_expansion"],
+            "traffic": None,
+            "traffic_note": "no HBM-bound work: ncu DRAM bytes at 2^26 = "
+                            f"{(met['dram__bytes_read.sum'] + met['dram__bytes_write.sum']) / met['expansions']:.2f} B "
+                            "per expansion (the write-through stack, mostly absorbed by L2)",
+            "ncu": {k: met[k] for k in ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+                                         "smsp__issue_active.avg.pct_of_peak_sustained_active",
+                                         "sm__warps_active.avg.pct_of_peak_sustained_active")},
+            "source": "profiles/r02_prune3_metrics.json"}
+
+
+def measure(ctx, stream, *, rows_log2: int = 13, prune_log2: int = 26, depth: int = 3000, walk_log2: int = 14,
+            cpu_sample: int = 1 << 14, keep=None, lop3_peak=None) -> dict:
     """Config 3 on one GPU: K2 over 2^rows_log2 R2 rows (the 2^32-state slice by default),
     K3 (DFS, `depth`) on the first 2^prune_log2 candidates, K1 on a prefix of the
     survivors; each with parity against the C restatement on a sample and a CPU baseline.
@@ -143,9 +176,14 @@ def measure(ctx, stream, *, rows_log2: int = 13, prune_log2: int = 24, depth: in
     cpu_s = time.perf_counter() - t0
     k3_parity = bool((o_removed == removed.cpu().numpy()[idx]).all() and
                      (o_work == work.cpu().numpy().view(np.uint64)[idx]).all())
+    if lop3_peak is None:
+        lop3_peak = N.lop3_peak(ctx.device)
     k3 = {"candidates": npr, "depth_limit": depth, "removed": nremoved, "removed_fraction": nremoved / npr,
           "expanded": expanded, "seconds": k3_s, "candidates_per_s": npr / k3_s,
-          "expansions_per_s": expanded / k3_s, "parity_sample_vs_oracle": k3_parity,
+          "expansions_per_s": expanded / k3_s,
+          "roofline": k3_roofline(expanded / k3_s, lop3_peak[0], lop3_peak[1]),
+          "kernel": "prune3_kernel (K3 v3, csrc/prune.cu)",
+          "parity_sample_vs_oracle": k3_parity,
           "parity_sample": int(idx.size),
           "cpu_baseline": {"value": float(o_work.sum()) / cpu_s, "unit": "expansions/s", "cores": cores,
                            "kind": "port", "sample": f"{idx.size} evenly spaced candidates of the {npr} "
@@ -165,7 +203,7 @@ def measure(ctx, stream, *, rows_log2: int = 13, prune_log2: int = 24, depth: in
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rows-log2", type=int, default=13)   # 2^13 rows x (2^19-1) = 2^32 states
-    ap.add_argument("--prune-log2", type=int, default=20)
+    ap.add_argument("--prune-log2", type=int, default=26)
     ap.add_argument("--depth", type=int, default=3000)     # the paper's DFS depth
     ap.add_argument("--walk-log2", type=int, default=14)
     ap.add_argument("--full", action="store_true")
