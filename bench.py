@@ -243,7 +243,10 @@ def main() -> None:
         local = 0
     torch.cuda.set_device(local)
     nccl = None
-    if world > 1:
+    # LFSR_BENCH_NCCL=1 (testing only): a one-rank NCCL communicator under torchrun, so the
+    # NCCL data plane (statistics all-reduce, max-over-ranks timing) runs on a one-GPU box
+    force_nccl = os.environ.get("LFSR_BENCH_NCCL") == "1" and "RANK" in os.environ
+    if world > 1 or force_nccl:
         if share:
             dist.init_process_group("gloo")
         else:
@@ -253,6 +256,8 @@ def main() -> None:
             if rank == 0:
                 print(f"[bench] NCCL communicator: {nccl['world_size']} ranks, NCCL {nccl['nccl_version']}",
                       file=sys.stderr, flush=True)
+
+    multi = world > 1 or nccl is not None  # collectives run (a one-rank NCCL communicator too)
 
     import paper_1210_6411_b200 as lc
     from paper_1210_6411_b200 import _native as N
@@ -319,7 +324,7 @@ def main() -> None:
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     e_all0, e_all1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
+    if multi:
         dist.barrier()
     torch.cuda.synchronize()
     N.launch_count_reset()
@@ -333,7 +338,7 @@ def main() -> None:
         e_all1.record(stream)
         torch.cuda.synchronize()
     launches = N.launch_count()
-    if world > 1:
+    if multi:
         dist.barrier()
     elapsed = e_all0.elapsed_time(e_all1) / 1e3
     kernel_s = [a.elapsed_time(b) / 1e3 for a, b in ev]
@@ -342,9 +347,9 @@ def main() -> None:
     local_stats = combine_stats([stats[k].cpu().numpy().view(np.uint64) for k in range(args.steps)])
     if int(local_stats[N.ST_ERROR]):
         raise SystemExit(f"walk error {int(local_stats[N.ST_ERROR])}")
-    glob = allreduce_stats(local_stats, offset=rank * per_gpu) if world > 1 else local_stats
+    glob = allreduce_stats(local_stats, offset=rank * per_gpu) if multi else local_stats
     t_max = elapsed
-    if world > 1:
+    if multi:
         t = torch.tensor([elapsed], dtype=torch.float64, device=dev if nccl else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_max = float(t.item())
@@ -403,7 +408,7 @@ def main() -> None:
         e2e_el = 0.0
         e2e_match = []
         d_all = dst.view(torch.int64)
-        if world > 1:
+        if multi:
             dist.barrier()
         for k in range(args.steps):
             b = k % nbatches
@@ -417,7 +422,7 @@ def main() -> None:
             if k < nbatches:  # the host-buffer results equal the device path's, batch by batch
                 o = b * batch * LEGS
                 e2e_match.append(bool((h_dst == d_all[o:o + batch * LEGS].cpu().numpy().view(np.uint64)).all()))
-        if world > 1:
+        if multi:
             t = torch.tensor([e2e_el], dtype=torch.float64, device=dev if nccl else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_el = float(t.item())
@@ -513,7 +518,7 @@ def main() -> None:
             "steps12": steps12,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if multi:
         dist.destroy_process_group()
 
 
