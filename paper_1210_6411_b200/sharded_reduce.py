@@ -113,7 +113,10 @@ class _Exchange:
         import torch.distributed as dist
 
         self.torch, self.dist, self.group = torch, dist, group
-        if dist.is_available() and dist.is_initialized():
+        # with a process group (even of one rank) every exchange is a real collective;
+        # without one the exchanges are identities
+        self.solo = not (dist.is_available() and dist.is_initialized())
+        if not self.solo:
             self.world = dist.get_world_size(group)
             self.rank = dist.get_rank(group)
             self.nccl = dist.get_backend(group) == "nccl"
@@ -122,7 +125,7 @@ class _Exchange:
 
     def allgather(self, vec) -> np.ndarray:
         v = np.asarray(vec, dtype=np.int64)
-        if self.world == 1:
+        if self.solo:
             return v[None, :].copy()
         torch = self.torch
         dev = torch.device("cuda", torch.cuda.current_device()) if self.nccl else torch.device("cpu")
@@ -132,7 +135,7 @@ class _Exchange:
         return np.stack([o.cpu().numpy() for o in out])
 
     def alltoallv(self, send, send_counts, recv_counts):
-        if self.world == 1:
+        if self.solo:
             return send
         torch = self.torch
         staged = send.is_cuda and not self.nccl

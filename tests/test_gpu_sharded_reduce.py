@@ -84,11 +84,16 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, backend="gloo"):
+    import torch
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if backend == "nccl":
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_1210_6411_b200.distributed import shard_range
         from paper_1210_6411_b200.sharded_reduce import cut_leaves_sharded
@@ -117,6 +122,21 @@ def test_sharded_two_ranks_on_one_gpu(gpu):
         assert rows == np.stack(want[:5], 1).tolist(), name
         for r in range(world):
             assert out[(name, r)][1] == [tuple(int(v) for v in p) for p in want[5]], name
+
+
+def test_sharded_one_rank_over_nccl(gpu):
+    """The per-pass all-gather and all-to-all through a real NCCL communicator (one rank:
+    this box has one GPU; a multi-GPU node runs the same calls with N ranks)."""
+    import torch.multiprocessing as mp
+    from oracle import reduce_np
+
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(1, _free_port(), out, "nccl"), nprocs=1, join=True)
+    for name, cols in {"mini789": _mini789(), "random": _random_mapping(1 << 16, 5)}.items():
+        want = reduce_np.cut_leaves(*cols)
+        assert out[(name, 0)][0] == np.stack(want[:5], 1).tolist(), name
+        assert out[(name, 0)][1] == [tuple(int(v) for v in p) for p in want[5]], name
 
 
 def _shaped(kind, n, seed):
