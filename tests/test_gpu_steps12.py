@@ -241,7 +241,7 @@ ok = ok and (removed == np.asarray(o_removed).astype(bool)).all() and (work == n
 print(json.dumps({"ok": bool(ok)}))
 '''
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, LFSR_PRUNE_SPILL=spill, LFSR_PRUNE_RING=ring)
+    env = dict(os.environ, LFSR_PRUNE_SPILL=spill, LFSR_PRUNE_RING=ring, LFSR_PRUNE_V1="2")  # v2's fallback
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert json.loads(r.stdout.strip().splitlines()[-1])["ok"]
@@ -265,16 +265,17 @@ def test_enumerate_overflow_returns_prefix(gpu, lc, specs, params):
         assert (out == full[:cap]).all(), cap
 
 
-@pytest.mark.parametrize("ring", ["32", "20"])
-def test_prune_random_configs_match_restatement(gpu, lc, specs, params, ring, monkeypatch):
+@pytest.mark.parametrize("kernel", ["v3", "v2", "v1"])
+def test_prune_random_configs_match_restatement(gpu, lc, specs, params, kernel, monkeypatch):
     """Seeded random (cipher, mode, limit, candidate subset) configurations: removed flags
     and per-candidate `expanded` counters equal the C restatement's (pinned to the
-    reference by prune.json) -- including limits around the ring's depth field and
-    node limits that cut traversals mid-way -- for both ring variants (the launch reads
-    LFSR_PRUNE_RING)."""
+    reference by prune.json) -- including limits around v2's 12-bit depth field and v3's
+    4096 cut-over, and node limits that cut traversals mid-way -- for each kernel (the
+    launch reads LFSR_PRUNE_V1: unset = v3 for DFS up to 4096, 2 = v2, 1 = round 1)."""
     import random
 
-    monkeypatch.setenv("LFSR_PRUNE_RING", ring)
+    if kernel != "v3":
+        monkeypatch.setenv("LFSR_PRUNE_V1", kernel[1])
     from oracle import port
     from paper_1210_6411_b200 import _batch
 
