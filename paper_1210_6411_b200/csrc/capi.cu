@@ -760,15 +760,17 @@ int lc_prune_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int32_t
     LC_CUDA(lc::launch_prune(id, static_cast<uint32_t>(fixed_r3), mode, limit, d_cands, n, d_removed, d_work,
                              ctx->pq.as<unsigned long long>(), spill_cap ? ctx->spill.p : nullptr, spill_cap, ring,
                              blocks, st));
-  } else if (mode == 0 && limit <= lc::prune3_max_limit() && !(v1 && v1[0] == '2')) {
-    // DFS: the uniform-step kernel (LFSR_PRUNE_V1=2 selects the v2 kernel for A/B); the
-    // grid is capped by the batch so small batches do not allocate every lane's spill stack
+  } else if (limit <= lc::prune3_max_limit() && !(v1 && v1[0] == '2')) {
+    // the uniform-step kernel (LFSR_PRUNE_V1=2 selects the v2 kernel for A/B); a stack
+    // holds at most `limit` entries in either mode (DFS: ancestors at distinct depths <=
+    // limit; BFS: the traversal stops past `limit` nodes); the grid is capped by the
+    // batch so small batches do not allocate every lane's stack
     const uint64_t lanes_max = (n + 31) / 32 * 32;
     int blocks = lc::prune3_blocks_per_sm(id) * ctx->sms;
     const uint64_t need_blocks = (lanes_max + lc::prune3_threads() - 1) / lc::prune3_threads();
     if (static_cast<uint64_t>(blocks) > need_blocks) blocks = static_cast<int>(need_blocks);
     LC_CUDA(ctx->spill.ensure(lc::prune3_spill_bytes(blocks, static_cast<uint32_t>(limit))));
-    LC_CUDA(lc::launch_prune3(id, static_cast<uint32_t>(fixed_r3), static_cast<uint32_t>(limit), d_cands, n,
+    LC_CUDA(lc::launch_prune3(id, static_cast<uint32_t>(fixed_r3), mode, static_cast<uint32_t>(limit), d_cands, n,
                               d_removed, d_work, ctx->pq.as<unsigned long long>(), ctx->spill.p, blocks, st));
   } else {
     const int blocks = lc::prune2_blocks_per_sm(id, mode) * ctx->sms;

@@ -150,14 +150,14 @@ cudaError_t launch_prune2(SpecId id, uint32_t F, int mode, uint64_t limit, const
                           uint8_t* removed, uint64_t* work, unsigned long long* queue, void* spill,
                           uint32_t spill_cap, int blocks, cudaStream_t stream);
 
-// K3 v3 (csrc/prune.cu): DFS mode, one uniform step per expansion, a per-lane stack that
-// never drops entries (spill: prune3_spill_bytes(blocks, limit) bytes); for limit <=
-// prune3_max_limit().  Same results as launch_prune2 (mode 0).
+// K3 v3 (csrc/prune.cu): one uniform step per expansion, a per-lane stack that never
+// drops entries (spill: prune3_spill_bytes(blocks, limit) bytes); for limit <=
+// prune3_max_limit().  Same results as launch_prune2; mode 0 = dfs, 1 = bfs.
 int prune3_blocks_per_sm(SpecId id);
 int prune3_threads();
 uint32_t prune3_max_limit();
 uint64_t prune3_spill_bytes(int blocks, uint32_t limit);
-cudaError_t launch_prune3(SpecId id, uint32_t F, uint32_t limit, const uint64_t* cands, uint64_t n,
+cudaError_t launch_prune3(SpecId id, uint32_t F, int mode, uint32_t limit, const uint64_t* cands, uint64_t n,
                           uint8_t* removed, uint64_t* work, unsigned long long* queue, void* spill, int blocks,
                           cudaStream_t stream);
 

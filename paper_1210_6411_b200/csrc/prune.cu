@@ -654,7 +654,7 @@ __device__ __forceinline__ void cp_async16(uint32_t smem, const void* g) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-template <class S, int K>
+template <class S, int K, bool DFS>
 __global__ void __launch_bounds__(kThreads3) prune3_kernel(const uint64_t* __restrict__ cands, uint64_t n,
                                                            uint32_t F, uint32_t limit,
                                                            uint8_t* __restrict__ removed,
@@ -692,7 +692,7 @@ __global__ void __launch_bounds__(kThreads3) prune3_kernel(const uint64_t* __res
           if (i < n) {
             unpack2<S>(cands[i], r1, r2, r3);
             d = 0;
-            acc = 0;
+            acc = DFS ? 0 : 1;  // BFS counts the root (pipeline.py:149)
             sp = lo = 0;
             have = true;
           }
@@ -705,11 +705,22 @@ __global__ void __launch_bounds__(kThreads3) prune3_kernel(const uint64_t* __res
       const uint32_t m = child_set3<S>(tbl, r1, r2, r3, F);
       const bool leaf = m == 0u;
       int fin = 0;  // 1 removed (traversal complete), 2 survivor (a child below the limit)
-      if (!leaf && d >= limit) {  // pipeline.py:138-141: the first child counts, then abort
-        acc += 1;
-        fin = 2;
-      } else if (leaf && sp == 0u) {
-        fin = 1;
+      if (DFS) {
+        if (!leaf && d >= limit) {  // pipeline.py:138-141: the first child counts, then abort
+          acc += 1;
+          fin = 2;
+        } else if (leaf && sp == 0u) {
+          fin = 1;
+        }
+      } else {
+        // BFS (pipeline.py:147-160) counts nodes until the count passes the limit; both
+        // outcomes are independent of the visiting order, so the DFS order serves
+        if (acc + __popc(m) > limit) {
+          acc = static_cast<uint64_t>(limit) + 1;
+          fin = 2;
+        } else if (leaf && sp == 0u) {
+          fin = 1;
+        }
       }
       if (fin != 0) {
         LC_CHECK(i < n);
@@ -794,9 +805,10 @@ int blocks2(bool dfs) {
 }
 
 template <class S>
-const void* kernel3() {
+const void* kernel3(bool dfs) {
   // (per call: the attribute is per device, and setting it is a cheap host call)
-  const void* k = reinterpret_cast<const void*>(prune3_kernel<S, kStack3>);
+  const void* k = dfs ? reinterpret_cast<const void*>(prune3_kernel<S, kStack3, true>)
+                      : reinterpret_cast<const void*>(prune3_kernel<S, kStack3, false>);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kStack3Bytes);
   return k;
 }
@@ -804,7 +816,7 @@ const void* kernel3() {
 template <class S>
 int blocks3() {
   int b = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel3<S>(), kThreads3, kStack3Bytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel3<S>(true), kThreads3, kStack3Bytes);
   return b > 0 ? b : 1;
 }
 
@@ -853,19 +865,19 @@ uint64_t prune3_spill_bytes(int blocks, uint32_t limit) {
   return static_cast<uint64_t>(blocks) * kThreads3 * limit * sizeof(uint4);
 }
 
-cudaError_t launch_prune3(SpecId id, uint32_t F, uint32_t limit, const uint64_t* cands, uint64_t n,
+cudaError_t launch_prune3(SpecId id, uint32_t F, int mode, uint32_t limit, const uint64_t* cands, uint64_t n,
                           uint8_t* removed, uint64_t* work, unsigned long long* queue, void* spill, int blocks,
                           cudaStream_t stream) {
   uint4* sp = static_cast<uint4*>(spill);
   const void* k = nullptr;
   switch (id) {
-    case SpecId::A51: k = kernel3<A51>(); break;
-    case SpecId::MINI567: k = kernel3<MINI567>(); break;
-    case SpecId::MINI789: k = kernel3<MINI789>(); break;
+    case SpecId::A51: k = kernel3<A51>(mode == 0); break;
+    case SpecId::MINI567: k = kernel3<MINI567>(mode == 0); break;
+    case SpecId::MINI789: k = kernel3<MINI789>(mode == 0); break;
     case SpecId::CUSTOM: {
       const CustomKernels* c = current_custom();
       if (!c) return cudaErrorInvalidValue;
-      k = reinterpret_cast<const void*>(c->prune3_dfs);
+      k = reinterpret_cast<const void*>(mode == 0 ? c->prune3_dfs : c->prune3_bfs);
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kStack3Bytes);
       break;
     }
