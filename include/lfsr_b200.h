@@ -280,6 +280,26 @@ int lc_bf_segments_device(lc_ctx *ctx, uint64_t n, const int64_t *d_succ, const 
                           const uint8_t *d_is_cand, const int64_t *d_cand, uint64_t ncand, int64_t *d_root,
                           int32_t *d_depth, uint64_t *level_counts, uint32_t level_cap, uint32_t *n_levels,
                           void *stream);
+/* The candidate ranks, ascending (ordered compaction of is_cand); *m_out = their count.
+ * Synchronous. */
+int lc_bf_candidates_device(lc_ctx *ctx, uint64_t n, const uint8_t *d_is_cand, int64_t *d_cand,
+                            uint64_t *m_out, void *stream);
+/* pred_hist[k] (5 entries, device) = states with k predecessors; per candidate index j <
+ * m: seg_depth[j] = deepest level of its segment, seg_size[j] = its states (from the
+ * segment sweep's root / depth). */
+int lc_bf_summary_device(lc_ctx *ctx, uint64_t n, const int32_t *d_indeg, const int64_t *d_root,
+                         const int32_t *d_depth, uint64_t m, uint64_t *d_pred_hist, int64_t *d_seg_depth,
+                         int64_t *d_seg_size, void *stream);
+/* The cycles of the functional graph (oracle.py:168-186, 254-283), from the successor map
+ * and cycle_of (lc_bf_build_device).  Cycles are numbered by their smallest on-cycle rank
+ * (ascending); cycle c's on-cycle ranks in walk order from that rank are
+ * order[offset[c] .. offset[c] + length[c]); leader[c] = its smallest packed state,
+ * cand_on[c] = candidates on it, comp[c] = states of its component.  Every output holds
+ * n entries (only *n_on, resp. *n_cycles, are written).  Synchronous. */
+int lc_bf_cycles_device(lc_ctx *ctx, const lc_spec *spec, uint64_t n, const int64_t *d_succ,
+                        const int64_t *d_cycle_of, const uint8_t *d_is_cand, int64_t *d_order, int64_t *d_offset,
+                        int64_t *d_length, int64_t *d_leader, int64_t *d_cand_on, int64_t *d_comp,
+                        uint64_t *n_on, uint64_t *n_cycles, void *stream);
 /* Cycles of a permutation of m compact indices (cs[i] = successor's index; indices in
  * ascending state order): start[i] = smallest index on i's cycle, steps[i] = steps from
  * i forward to it. */

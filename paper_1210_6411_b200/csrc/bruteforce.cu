@@ -1,10 +1,10 @@
 // Exhaustive functional-graph analysis of a mini cipher on the GPU: the reference's
 // ground-truth oracle (oracle.brute_force_analysis, oracle.py:141-283), SURVEY.md §8(f)
-// rank 4.  States are rank-encoded as in the reference (rank = ((r1-1)*m2 + (r2-1))*m3 +
+// rank 4.  Everything is in-house: the scans and ordered compactions below replace the
+// library scan and the tensor-library unique / searchsorted / bincount glue.  States are rank-encoded as in the reference (rank = ((r1-1)*m2 + (r2-1))*m3 +
 // (r3-1), oracle.py:55-63, 116-138).  Like the reference, the reverse direction comes
 // from inverting the successor map (a CSR built by counting sort), not from the
 // predecessor table.
-#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -27,6 +27,117 @@ inline unsigned grid_of(uint64_t n) {
 #define BF_LOOP(i, n)                                                                      \
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < (n); \
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+
+// ------------------------------------------------ scan and ordered compaction
+// Exclusive prefix sums of n values (u8 flags, i32 or i64 counts) into i64, three
+// launches: per-block totals, one block scanning the totals (in 2048-entry chunks,
+// carrying the running sum), per-block rescans adding the block's offset.  total[0]
+// receives the grand total.
+constexpr int kScanT = 256, kScanItems = 8, kScanTile = kScanT * kScanItems;
+
+__device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* warp_tot, int64_t* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[w] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t run = 0;
+    for (int i = 0; i < kScanT / 32; ++i) {
+      const int64_t t = warp_tot[i];
+      warp_tot[i] = run;
+      run += t;
+    }
+    *total = run;
+  }
+  __syncthreads();
+  const int64_t r = warp_tot[w] + x - v;
+  __syncthreads();
+  return r;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kScanT) scan_reduce_kernel(const T* __restrict__ in, uint64_t n,
+                                                             int64_t* __restrict__ block_sums) {
+  __shared__ int64_t wt[kScanT / 32], tot;
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+  int64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k)
+    if (base + k < n) s += static_cast<int64_t>(in[base + k]);
+  block_excl_scan(s, wt, &tot);
+  if (threadIdx.x == 0) block_sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanT) scan_blocks_kernel(int64_t* __restrict__ sums, uint64_t nb,
+                                                             int64_t* __restrict__ total) {
+  __shared__ int64_t wt[kScanT / 32], tot;
+  int64_t carry = 0;
+  for (uint64_t c = 0; c < nb; c += kScanTile) {
+    const uint64_t base = c + threadIdx.x * kScanItems;
+    int64_t v[kScanItems], s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      v[k] = base + k < nb ? sums[base + k] : 0;
+      s += v[k];
+    }
+    int64_t run = carry + block_excl_scan(s, wt, &tot);
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k)
+      if (base + k < nb) {
+        sums[base + k] = run;
+        run += v[k];
+      }
+    carry += tot;
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kScanT) scan_down_kernel(const T* __restrict__ in, uint64_t n,
+                                                           const int64_t* __restrict__ block_sums,
+                                                           int64_t* __restrict__ out) {
+  __shared__ int64_t wt[kScanT / 32], tot;
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+  int64_t v[kScanItems], s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    v[k] = base + k < n ? static_cast<int64_t>(in[base + k]) : 0;
+    s += v[k];
+  }
+  int64_t run = block_sums[blockIdx.x] + block_excl_scan(s, wt, &tot);
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k)
+    if (base + k < n) {
+      out[base + k] = run;
+      run += v[k];
+    }
+}
+
+uint64_t scan_blocks(uint64_t n) { return (n + kScanTile - 1) / kScanTile; }
+
+// out[i] = sum(in[0..i)); *d_total = sum(in).  block_sums: scan_blocks(n) entries.
+template <class T>
+cudaError_t excl_scan(const T* in, uint64_t n, int64_t* out, int64_t* block_sums, int64_t* d_total, cudaStream_t st,
+                      int* launches) {
+  if (n == 0) return cudaMemsetAsync(d_total, 0, 8, st);
+  const uint64_t nb = scan_blocks(n);
+  scan_reduce_kernel<T><<<static_cast<unsigned>(nb), kScanT, 0, st>>>(in, n, block_sums);
+  scan_blocks_kernel<<<1, kScanT, 0, st>>>(block_sums, nb, d_total);
+  scan_down_kernel<T><<<static_cast<unsigned>(nb), kScanT, 0, st>>>(in, n, block_sums, out);
+  *launches += 3;
+  return cudaGetLastError();
+}
+
+// ordered compaction: out[pos[i]] = i for the flagged i (pos = exclusive scan of flags)
+__global__ void compact_kernel(const uint8_t* __restrict__ flag, const int64_t* __restrict__ pos, uint64_t n,
+                               int64_t* __restrict__ out) {
+  BF_LOOP(i, n) if (flag[i]) out[pos[i]] = static_cast<int64_t>(i);
+}
 
 // oracle.py:116-138 _build_successors (majority rule, or every register clocked)
 template <class S>
@@ -167,6 +278,77 @@ __global__ void bf_edges_kernel(const int64_t* __restrict__ cand, uint64_t m, co
   }
 }
 
+// pred_hist[k] = states with k predecessors; per candidate index: segment depth (max)
+// and size (oracle.py:238-252)
+__global__ void bf_summary_kernel(const int32_t* __restrict__ indeg, const int64_t* __restrict__ root,
+                                  const int32_t* __restrict__ depth, uint64_t n,
+                                  unsigned long long* __restrict__ pred_hist, unsigned long long* __restrict__ seg_depth,
+                                  unsigned long long* __restrict__ seg_size) {
+  __shared__ unsigned int h[5];
+  if (threadIdx.x < 5) h[threadIdx.x] = 0;
+  __syncthreads();
+  BF_LOOP(x, n) {
+    const int32_t k = indeg[x];
+    LC_CHECK(k >= 0 && k <= 4);
+    atomicAdd(&h[k], 1u);
+    const int64_t r = root[x];
+    if (r >= 0) {
+      atomicMax(&seg_depth[r], static_cast<unsigned long long>(depth[x]));
+      atomicAdd(&seg_size[r], 1ull);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 5 && h[threadIdx.x]) atomicAdd(&pred_hist[threadIdx.x], static_cast<unsigned long long>(h[threadIdx.x]));
+}
+
+__global__ void bf_mark_kernel(const int64_t* __restrict__ g, uint64_t n, uint8_t* __restrict__ flag) {
+  BF_LOOP(x, n) flag[g[x]] = 1;
+}
+
+// successor of each on-cycle state as a compact (ascending-rank) index
+__global__ void bf_cs_kernel(const int64_t* __restrict__ cyc, uint64_t m, const int64_t* __restrict__ succ,
+                             const int64_t* __restrict__ pos, int64_t* __restrict__ cs) {
+  BF_LOOP(k, m) cs[k] = pos[succ[cyc[k]]];
+}
+
+__global__ void bf_is_start_kernel(const int64_t* __restrict__ start, uint64_t m, uint8_t* __restrict__ flag) {
+  BF_LOOP(k, m) flag[k] = start[k] == static_cast<int64_t>(k) ? 1 : 0;
+}
+
+// per cycle c (numbered by ascending start rank): length, candidates on it, leader (the
+// smallest packed state on it), and each on-cycle state's cycle
+__global__ void bf_cycle_stats_kernel(const int64_t* __restrict__ cyc, const int64_t* __restrict__ start,
+                                      const int64_t* __restrict__ pos2, uint64_t m, const uint8_t* __restrict__ is_cand,
+                                      uint64_t m2, uint64_t m3, int o2, int o3, int64_t* __restrict__ cid,
+                                      unsigned long long* __restrict__ length, unsigned long long* __restrict__ cand_on,
+                                      unsigned long long* __restrict__ leader, int64_t* __restrict__ cycle_of_state) {
+  BF_LOOP(k, m) {
+    const int64_t c = pos2[start[k]];
+    const uint64_t x = static_cast<uint64_t>(cyc[k]);
+    cid[k] = c;
+    cycle_of_state[x] = c;
+    atomicAdd(&length[c], 1ull);
+    if (is_cand[x]) atomicAdd(&cand_on[c], 1ull);
+    const uint64_t r1 = x / m3 / m2 + 1, r2 = (x / m3) % m2 + 1, r3 = x % m3 + 1;
+    atomicMin(&leader[c], r1 | (r2 << o2) | (r3 << o3));
+  }
+}
+
+// walk order from each cycle's start: position (length - steps) mod length
+__global__ void bf_order_kernel(const int64_t* __restrict__ cyc, const int64_t* __restrict__ cid,
+                                const int64_t* __restrict__ steps, uint64_t m, const int64_t* __restrict__ length,
+                                const int64_t* __restrict__ offset, int64_t* __restrict__ order) {
+  BF_LOOP(k, m) {
+    const int64_t c = cid[k], L = length[c];
+    order[offset[c] + (L - steps[k]) % L] = cyc[k];
+  }
+}
+
+__global__ void bf_comp_kernel(const int64_t* __restrict__ g, uint64_t n, const int64_t* __restrict__ cycle_of_state,
+                               unsigned long long* __restrict__ comp) {
+  BF_LOOP(x, n) atomicAdd(&comp[cycle_of_state[g[x]]], 1ull);
+}
+
 template <class S>
 cudaError_t build_t(uint64_t n, int clock_all, uint32_t F, int64_t* succ, int32_t* indeg, uint8_t* is_cand,
                     int64_t* g, int64_t* tmp, cudaStream_t st, int* launches) {
@@ -209,10 +391,7 @@ cudaError_t bf_edges(uint64_t n, const int64_t* succ, const uint8_t* is_cand, co
 }
 
 size_t bf_segments_scratch(uint64_t n) {
-  size_t temp = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, temp, static_cast<const int32_t*>(nullptr), static_cast<int64_t*>(nullptr),
-                                static_cast<int64_t>(n + 1));
-  return temp + (n + 1) * 8 + n * 4 + n * 8 * 3 + 16 * 256;
+  return (scan_blocks(n) + 1) * 8 + (n + 1) * 8 + n * 4 + n * 8 * 3 + 16 * 256;
 }
 
 cudaError_t bf_segments(uint64_t n, const int64_t* succ, const int32_t* indeg, const uint8_t* is_cand,
@@ -231,16 +410,12 @@ cudaError_t bf_segments(uint64_t n, const int64_t* succ, const int32_t* indeg, c
   int64_t* fa = reinterpret_cast<int64_t*>(take(n * 8));
   int64_t* fb = reinterpret_cast<int64_t*>(take(n * 8));
   unsigned long long* cnt = reinterpret_cast<unsigned long long*>(take(256));
-  void* temp = base;
-  size_t temp_bytes = scratch_bytes - static_cast<size_t>(base - static_cast<uint8_t*>(scratch));
+  int64_t* bsums = reinterpret_cast<int64_t*>(take(scan_blocks(n) * 8));
+  (void)scratch_bytes;
   cudaError_t e;
-  // CSR of predecessors: offsets = exclusive scan of the in-degrees (n + 1 entries, the
-  // last in-degree read as 0 through a zeroed cursor slot is not needed: scan n, then
-  // offsets[n] = n since every state has exactly one successor)
-  e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, indeg, offsets, static_cast<int64_t>(n), st);
-  if (e != cudaSuccess) return e;
-  const int64_t total = static_cast<int64_t>(n);
-  if ((e = cudaMemcpyAsync(offsets + n, &total, 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) return e;
+  // CSR of predecessors: offsets = exclusive scan of the in-degrees, offsets[n] = their
+  // total (= n: every state has exactly one successor)
+  if ((e = excl_scan(indeg, n, offsets, bsums, offsets + n, st, launches)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(cursor, 0, n * 4, st)) != cudaSuccess) return e;
   bf_scatter_preds_kernel<<<grid_of(n), kT, 0, st>>>(succ, n, offsets, cursor, preds);
   if ((e = cudaMemsetAsync(root, 0xff, n * 8, st)) != cudaSuccess) return e;
@@ -265,6 +440,109 @@ cudaError_t bf_segments(uint64_t n, const int64_t* succ, const int32_t* indeg, c
     std::swap(fa, fb);
   }
   *n_levels = levels;
+  return cudaGetLastError();
+}
+
+size_t bf_candidates_scratch(uint64_t n) { return (scan_blocks(n) + 2) * 8 + n * 8 + 1024; }
+
+cudaError_t bf_candidates(uint64_t n, const uint8_t* is_cand, int64_t* cand, uint64_t* m_out, void* scratch,
+                          cudaStream_t st, int* launches) {
+  int64_t* pos = static_cast<int64_t*>(scratch);
+  int64_t* tot = pos + n;
+  int64_t* bs = tot + 2;
+  cudaError_t e;
+  if ((e = excl_scan(is_cand, n, pos, bs, tot, st, launches)) != cudaSuccess) return e;
+  compact_kernel<<<grid_of(n), kT, 0, st>>>(is_cand, pos, n, cand);
+  ++*launches;
+  int64_t h = 0;
+  if ((e = cudaMemcpyAsync(&h, tot, 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  *m_out = static_cast<uint64_t>(h);
+  return cudaGetLastError();
+}
+
+cudaError_t bf_summary(uint64_t n, const int32_t* indeg, const int64_t* root, const int32_t* depth, uint64_t m,
+                       uint64_t* pred_hist, int64_t* seg_depth, int64_t* seg_size, cudaStream_t st, int* launches) {
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(pred_hist, 0, 5 * 8, st)) != cudaSuccess) return e;
+  if (m && (e = cudaMemsetAsync(seg_depth, 0, m * 8, st)) != cudaSuccess) return e;
+  if (m && (e = cudaMemsetAsync(seg_size, 0, m * 8, st)) != cudaSuccess) return e;
+  bf_summary_kernel<<<grid_of(n), kT, 0, st>>>(indeg, root, depth, n,
+                                               reinterpret_cast<unsigned long long*>(pred_hist),
+                                               reinterpret_cast<unsigned long long*>(seg_depth),
+                                               reinterpret_cast<unsigned long long*>(seg_size));
+  ++*launches;
+  return cudaGetLastError();
+}
+
+size_t bf_cycles_scratch(uint64_t n) { return n * 8 * 11 + n * 2 + (scan_blocks(n) + 4) * 8 + 4096; }
+
+cudaError_t bf_cycles(uint64_t n, const int64_t* succ, const int64_t* g, const uint8_t* is_cand, uint64_t m2,
+                      uint64_t m3, int o2, int o3, int64_t* order, int64_t* offset, int64_t* length, int64_t* leader,
+                      int64_t* cand_on, int64_t* comp, uint64_t* n_on, uint64_t* n_cycles, void* scratch,
+                      cudaStream_t st, int* launches) {
+  uint8_t* base = static_cast<uint8_t*>(scratch);
+  auto take = [&](size_t bytes) {
+    uint8_t* p = base;
+    base += (bytes + 255) & ~size_t(255);
+    return p;
+  };
+  int64_t* pos = reinterpret_cast<int64_t*>(take(n * 8));
+  int64_t* cyc = reinterpret_cast<int64_t*>(take(n * 8));
+  int64_t* cs = reinterpret_cast<int64_t*>(take(n * 8));
+  int64_t* start = reinterpret_cast<int64_t*>(take(n * 8));
+  int64_t* steps = reinterpret_cast<int64_t*>(take(n * 8));
+  int64_t* t0 = reinterpret_cast<int64_t*>(take(n * 8));
+  int64_t* t1 = reinterpret_cast<int64_t*>(take(n * 8));
+  int64_t* t2 = reinterpret_cast<int64_t*>(take(n * 8));
+  int64_t* pos2 = reinterpret_cast<int64_t*>(take(n * 8));
+  int64_t* cid = reinterpret_cast<int64_t*>(take(n * 8));
+  int64_t* cos = reinterpret_cast<int64_t*>(take(n * 8));
+  uint8_t* flag = take(n);
+  uint8_t* flag2 = take(n);
+  int64_t* tot = reinterpret_cast<int64_t*>(take(32));
+  int64_t* bs = reinterpret_cast<int64_t*>(take(scan_blocks(n) * 8));
+  cudaError_t e;
+  int64_t h = 0;
+  auto fetch = [&](const int64_t* d, int64_t* out) {
+    cudaError_t r = cudaMemcpyAsync(out, d, 8, cudaMemcpyDeviceToHost, st);
+    return r != cudaSuccess ? r : cudaStreamSynchronize(st);
+  };
+  // on-cycle states = the image of f^(2^k), ascending (oracle.py:168-186)
+  if ((e = cudaMemsetAsync(flag, 0, n, st)) != cudaSuccess) return e;
+  bf_mark_kernel<<<grid_of(n), kT, 0, st>>>(g, n, flag);
+  ++*launches;
+  if ((e = excl_scan(flag, n, pos, bs, tot, st, launches)) != cudaSuccess) return e;
+  compact_kernel<<<grid_of(n), kT, 0, st>>>(flag, pos, n, cyc);
+  ++*launches;
+  if ((e = fetch(tot, &h)) != cudaSuccess) return e;
+  const uint64_t m = static_cast<uint64_t>(h);
+  *n_on = m;
+  bf_cs_kernel<<<grid_of(m), kT, 0, st>>>(cyc, m, succ, pos, cs);
+  ++*launches;
+  if ((e = bf_cycle_order(m, cs, start, steps, t0, t1, t2, st, launches)) != cudaSuccess) return e;
+  // cycles numbered by their start (smallest index on the cycle)
+  bf_is_start_kernel<<<grid_of(m), kT, 0, st>>>(start, m, flag2);
+  ++*launches;
+  if ((e = excl_scan(flag2, m, pos2, bs, tot, st, launches)) != cudaSuccess) return e;
+  if ((e = fetch(tot, &h)) != cudaSuccess) return e;
+  const uint64_t nc = static_cast<uint64_t>(h);
+  *n_cycles = nc;
+  if (nc) {
+    if ((e = cudaMemsetAsync(length, 0, nc * 8, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(cand_on, 0, nc * 8, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(comp, 0, nc * 8, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(leader, 0xff, nc * 8, st)) != cudaSuccess) return e;  // u64 max
+  }
+  bf_cycle_stats_kernel<<<grid_of(m), kT, 0, st>>>(cyc, start, pos2, m, is_cand, m2, m3, o2, o3, cid,
+                                                   reinterpret_cast<unsigned long long*>(length),
+                                                   reinterpret_cast<unsigned long long*>(cand_on),
+                                                   reinterpret_cast<unsigned long long*>(leader), cos);
+  ++*launches;
+  if ((e = excl_scan(length, nc, offset, bs, tot, st, launches)) != cudaSuccess) return e;
+  bf_order_kernel<<<grid_of(m), kT, 0, st>>>(cyc, cid, steps, m, length, offset, order);
+  bf_comp_kernel<<<grid_of(n), kT, 0, st>>>(g, n, cos, reinterpret_cast<unsigned long long*>(comp));
+  *launches += 2;
   return cudaGetLastError();
 }
 

@@ -1114,6 +1114,61 @@ int lc_bf_segments_device(lc_ctx* ctx, uint64_t n, const int64_t* d_succ, const 
   return LC_OK;
 }
 
+int lc_bf_candidates_device(lc_ctx* ctx, uint64_t n, const uint8_t* d_is_cand, int64_t* d_cand, uint64_t* m_out,
+                            void* stream) {
+  if (!ctx || !m_out) return fail(LC_ERR_ARG, "null argument");
+  *m_out = 0;
+  if (n == 0) return LC_OK;
+  if (!d_is_cand || !d_cand) return fail(LC_ERR_ARG, "null buffer");
+  LC_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  Ordered ord_(ctx, st);
+  LC_CUDA(ctx->scratch.ensure(lc::bf_candidates_scratch(n)));
+  int launches = 0;
+  LC_CUDA(lc::bf_candidates(n, d_is_cand, d_cand, m_out, ctx->scratch.p, st, &launches));
+  g_launches += launches;
+  return LC_OK;
+}
+
+int lc_bf_summary_device(lc_ctx* ctx, uint64_t n, const int32_t* d_indeg, const int64_t* d_root,
+                         const int32_t* d_depth, uint64_t m, uint64_t* d_pred_hist, int64_t* d_seg_depth,
+                         int64_t* d_seg_size, void* stream) {
+  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  if (!d_pred_hist || (n && (!d_indeg || !d_root || !d_depth)) || (m && (!d_seg_depth || !d_seg_size)))
+    return fail(LC_ERR_ARG, "null buffer");
+  LC_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  int launches = 0;
+  LC_CUDA(lc::bf_summary(n, d_indeg, d_root, d_depth, m, d_pred_hist, d_seg_depth, d_seg_size, st, &launches));
+  g_launches += launches;
+  return LC_OK;
+}
+
+int lc_bf_cycles_device(lc_ctx* ctx, const lc_spec* spec, uint64_t n, const int64_t* d_succ, const int64_t* d_cycle_of,
+                        const uint8_t* d_is_cand, int64_t* d_order, int64_t* d_offset, int64_t* d_length,
+                        int64_t* d_leader, int64_t* d_cand_on, int64_t* d_comp, uint64_t* n_on, uint64_t* n_cycles,
+                        void* stream) {
+  if (!ctx || !n_on || !n_cycles) return fail(LC_ERR_ARG, "null argument");
+  lc::SpecId id;
+  int rc = check_spec(spec, &id);
+  if (rc) return rc;
+  if (n == 0 || n != valid_states(id)) return fail(LC_ERR_ARG, "n must be the spec's valid state count");
+  if (!d_succ || !d_cycle_of || !d_is_cand || !d_order || !d_offset || !d_length || !d_leader || !d_cand_on ||
+      !d_comp)
+    return fail(LC_ERR_ARG, "null buffer");
+  LC_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  Ordered ord_(ctx, st);
+  LC_CUDA(ctx->scratch.ensure(lc::bf_cycles_scratch(n)));
+  const uint64_t m2 = (1ull << spec->lengths[1]) - 1, m3 = (1ull << spec->lengths[2]) - 1;
+  const int o2 = spec->lengths[0], o3 = spec->lengths[0] + spec->lengths[1];
+  int launches = 0;
+  LC_CUDA(lc::bf_cycles(n, d_succ, d_cycle_of, d_is_cand, m2, m3, o2, o3, d_order, d_offset, d_length, d_leader,
+                        d_cand_on, d_comp, n_on, n_cycles, ctx->scratch.p, st, &launches));
+  g_launches += launches;
+  return LC_OK;
+}
+
 int lc_bf_cycle_order_device(lc_ctx* ctx, uint64_t m, const int64_t* d_cs, int64_t* d_start, int64_t* d_steps,
                              void* stream) {
   if (!ctx) return fail(LC_ERR_ARG, "null context");

@@ -222,6 +222,16 @@ cudaError_t bf_segments(uint64_t n, const int64_t* succ, const int32_t* indeg, c
                         int* launches);
 cudaError_t bf_cycle_order(uint64_t m, const int64_t* cs, int64_t* lab, int64_t* steps, int64_t* t0, int64_t* t1,
                            int64_t* t2, cudaStream_t st, int* launches);
+size_t bf_candidates_scratch(uint64_t n);
+cudaError_t bf_candidates(uint64_t n, const uint8_t* is_cand, int64_t* cand, uint64_t* m_out, void* scratch,
+                          cudaStream_t st, int* launches);
+cudaError_t bf_summary(uint64_t n, const int32_t* indeg, const int64_t* root, const int32_t* depth, uint64_t m,
+                       uint64_t* pred_hist, int64_t* seg_depth, int64_t* seg_size, cudaStream_t st, int* launches);
+size_t bf_cycles_scratch(uint64_t n);
+cudaError_t bf_cycles(uint64_t n, const int64_t* succ, const int64_t* g, const uint8_t* is_cand, uint64_t m2,
+                      uint64_t m3, int o2, int o3, int64_t* order, int64_t* offset, int64_t* length, int64_t* leader,
+                      int64_t* cand_on, int64_t* comp, uint64_t* n_on, uint64_t* n_cycles, void* scratch,
+                      cudaStream_t st, int* launches);
 
 size_t cycles_scratch_bytes(uint64_t n);
 cudaError_t count_cycles_device(uint64_t n, const uint64_t* src, const uint64_t* dst, const uint64_t* dist,

@@ -127,9 +127,11 @@ def brute_force_analysis(spec: CipherSpec, params: CandidateParams, *, clock_all
     g = torch.empty(n, **i64)
     N.check(N.lib.lc_bf_build_device(ctx.handle, C.byref(sspec), params.fixed_r3, int(bool(clock_all)), n,
                                      _ptr(succ), _ptr(indeg), _ptr(is_cand), _ptr(g), stream))
-    pred_hist = torch.bincount(indeg.long(), minlength=5)
-    cand = torch.nonzero(is_cand).flatten()  # ascending ranks
-    m = cand.numel()
+    cand = torch.empty(n, **i64)
+    mh = C.c_uint64(0)
+    N.check(N.lib.lc_bf_candidates_device(ctx.handle, n, _ptr(is_cand), _ptr(cand), C.byref(mh), stream))
+    m = int(mh.value)
+    cand = cand[:m]  # ascending ranks
 
     # candidate-graph edges
     edge_dst, edge_dist = torch.empty(m, **i64), torch.empty(m, **i64)
@@ -143,35 +145,23 @@ def brute_force_analysis(spec: CipherSpec, params: CandidateParams, *, clock_all
     nlev = C.c_uint32(0)
     N.check(N.lib.lc_bf_segments_device(ctx.handle, n, _ptr(succ), _ptr(indeg), _ptr(is_cand), _ptr(cand), m,
                                         _ptr(root), _ptr(depth), N.u64p(levels), cap, C.byref(nlev), stream))
-    assigned = root >= 0
-    if not clock_all and not bool(assigned.all()):
+    pred_hist = torch.empty(5, **i64)
+    seg_depth, seg_size = torch.empty(m, **i64), torch.empty(m, **i64)
+    N.check(N.lib.lc_bf_summary_device(ctx.handle, n, _ptr(indeg), _ptr(root), _ptr(depth), m, _ptr(pred_hist),
+                                       _ptr(seg_depth), _ptr(seg_size), stream))
+    if not clock_all and int(seg_size.sum().item()) != n:
         raise AssertionError("segment sweep missed states; graph is inconsistent")
-    seg_depth = torch.zeros(m, **i64)
-    seg_depth.scatter_reduce_(0, root[assigned], depth[assigned].long(), reduce="amax")
-    seg_size = torch.bincount(root[assigned], minlength=m)
 
-    # cycles: the on-cycle states are the image of f^(2^k); order each cycle from its
-    # smallest rank in walk order
-    cyc = torch.unique(g)  # ascending
-    cs = torch.searchsorted(cyc, succ[cyc])
-    start, steps = torch.empty_like(cyc), torch.empty_like(cyc)
-    N.check(N.lib.lc_bf_cycle_order_device(ctx.handle, cyc.numel(), _ptr(cs), _ptr(start), _ptr(steps), stream))
-    starts = torch.unique(start)                         # cycle k <-> its start index
-    cid = torch.searchsorted(starts, start)              # cycle of each on-cycle state
-    length = torch.bincount(cid, minlength=starts.numel())
-    pos = (length[cid] - steps) % length[cid]            # walk position from the start
-    offset = torch.cumsum(length, 0) - length
-    order = torch.empty_like(cyc)
-    order[offset[cid] + pos] = cyc
-    cycle_of_state = torch.full((n,), -1, **i64)
-    cycle_of_state[cyc] = cid
-    comp_sizes = torch.bincount(cycle_of_state[g], minlength=starts.numel())
-    cand_on = torch.bincount(cid, weights=is_cand[cyc].double(), minlength=starts.numel()).round().long()
-    m1, m2, m3 = spec.reg_masks
-    _, o2, o3 = spec.offsets
-    packed = ((cyc // m3 // m2 + 1) | (((cyc // m3) % m2 + 1) << o2) | ((cyc % m3 + 1) << o3))
-    leader = torch.full((starts.numel(),), np.iinfo(np.int64).max, **i64)
-    leader.scatter_reduce_(0, cid, packed, reduce="amin")
+    # cycles (on-cycle states = the image of f^(2^k)), each ordered from its smallest rank
+    # in walk order, with leader, candidates on it and component size
+    bufs = [torch.empty(n, **i64) for _ in range(6)]
+    order, offset, length, leader, cand_on, comp_sizes = bufs
+    n_on, n_cyc = C.c_uint64(0), C.c_uint64(0)
+    N.check(N.lib.lc_bf_cycles_device(ctx.handle, C.byref(sspec), n, _ptr(succ), _ptr(g), _ptr(is_cand),
+                                      *[_ptr(t) for t in bufs], C.byref(n_on), C.byref(n_cyc), stream))
+    k_cyc = int(n_cyc.value)
+    order = order[: int(n_on.value)]
+    offset, length, leader, cand_on, comp_sizes = (t[:k_cyc] for t in (offset, length, leader, cand_on, comp_sizes))
 
     h = lambda t: t.cpu().numpy()  # noqa: E731
     order_h, length_h, offset_h = h(order), h(length), h(offset)
@@ -179,7 +169,7 @@ def brute_force_analysis(spec: CipherSpec, params: CandidateParams, *, clock_all
     cand_h = h(cand)
     cycles = [CycleInfo(ranks=order_h[offset_h[k]:offset_h[k] + length_h[k]], leader=int(leader_h[k]),
                         clock_length=int(length_h[k]), candidate_count=int(cand_on_h[k]),
-                        component_size=int(comp_h[k])) for k in range(starts.numel())]
+                        component_size=int(comp_h[k])) for k in range(k_cyc)]
     return GroundTruth(spec=spec, params=params, node_count=n, succ=h(succ), pred_count_hist=h(pred_hist),
                        leaf_count=int(pred_hist[0]), cycles=cycles, cand_ranks=cand_h, edge_src=cand_h,
                        edge_dst=h(edge_dst), edge_dist=h(edge_dist), seg_depth=h(seg_depth), seg_size=h(seg_size),
