@@ -168,6 +168,15 @@ int lc_prune_device(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3, int32_t
 /* Seeded synthetic start set (K0): the first n special nodes of the
  * counter-based stream trial i -> (r1, r2) = split(splitmix64(seed + i*golden)), in trial
  * order.  *trials_used = trials consumed.  Host and device variants. */
+/* Replaces probe_segment (pipeline.py:262-298) for k roots at once: each root's reverse
+ * level-order sweep through its segment (predecessors that are not special nodes), as
+ * (deepest level reached, nodes seen, censored).  depth_cap / node_cap < 0: no cap.
+ * level_counts[l] (levels_cap entries, host) = nodes at depth l summed over the roots
+ * (index 0 = the roots).  Device-resident: one expand and one finalize launch per level,
+ * the host looking at the live count every 16 levels.  Synchronous. */
+int lc_probe_segments(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3, const uint64_t *roots, uint64_t k,
+                      int64_t depth_cap, int64_t node_cap, uint64_t *depth, uint64_t *nodes, uint8_t *censored,
+                      uint64_t *level_counts, uint32_t levels_cap);
 int lc_random_candidates(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3, uint64_t seed,
                          uint64_t n, uint64_t *out, uint64_t *trials_used);
 int lc_random_candidates_device(lc_ctx *ctx, const lc_spec *spec, uint64_t fixed_r3,

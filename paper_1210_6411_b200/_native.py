@@ -104,6 +104,8 @@ _SIGNATURES = {
     "lc_bf_segments_device": ([_vp, C.c_uint64, _vp, _vp, _vp, _vp, C.c_uint64, _vp, _vp, _u64p, C.c_uint32,
                                C.POINTER(C.c_uint32), _vp], C.c_int),
     "lc_bf_cycle_order_device": ([_vp, C.c_uint64, _vp, _vp, _vp, _vp], C.c_int),
+    "lc_probe_segments": ([_vp, C.POINTER(lc_spec), C.c_uint64, _u64p, C.c_uint64, C.c_int64, C.c_int64, _u64p, _u64p,
+                           C.POINTER(C.c_uint8), _u64p, C.c_uint32], C.c_int),
     "lc_bf_candidates_device": ([_vp, C.c_uint64, _vp, _vp, _u64p, _vp], C.c_int),
     "lc_bf_summary_device": ([_vp, C.c_uint64, _vp, _vp, _vp, C.c_uint64, _vp, _vp, _vp, _vp], C.c_int),
     "lc_bf_cycles_device": ([_vp, C.POINTER(lc_spec), C.c_uint64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

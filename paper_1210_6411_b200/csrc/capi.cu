@@ -802,6 +802,130 @@ int lc_prune(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int32_t mode, 
   return LC_OK;
 }
 
+// ------------------------------------------------------- batched segment probes
+
+int lc_probe_segments(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, const uint64_t* roots, uint64_t k,
+                      int64_t depth_cap, int64_t node_cap, uint64_t* depth, uint64_t* nodes, uint8_t* censored,
+                      uint64_t* level_counts, uint32_t levels_cap) {
+  if (!ctx) return fail(LC_ERR_ARG, "null context");
+  lc::SpecId id;
+  int rc = check_spec(spec, &id);
+  if (rc) return rc;
+  if ((rc = check_fixed(id, fixed_r3))) return rc;
+  if (k == 0) return LC_OK;
+  if (!roots || !depth || !nodes || !censored || (levels_cap && !level_counts)) return fail(LC_ERR_ARG, "null buffer");
+  if (k >= (1ull << 32)) return fail(LC_ERR_ARG, "too many roots");
+  LC_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  Ordered ord_(ctx, st);
+  const uint32_t kk = static_cast<uint32_t>(k);
+  // per-root state, counters, level counts
+  struct Ctl {
+    unsigned long long cnt[2], live[2], done;
+    unsigned int overflow;
+  };
+  const size_t per_root = 8 + 8 + 8 + 1;  // depth, nodes, lvl, status
+  LC_CUDA(ctx->d.ensure(k * per_root + 512 + static_cast<size_t>(levels_cap) * 8 + 64));
+  uint8_t* p = ctx->d.as<uint8_t>();
+  uint64_t* d_depth = reinterpret_cast<uint64_t*>(p);
+  uint64_t* d_nodes = d_depth + k;
+  unsigned long long* d_lvl = reinterpret_cast<unsigned long long*>(d_nodes + k);
+  Ctl* ctl = reinterpret_cast<Ctl*>(d_lvl + k);
+  unsigned long long* d_levels = reinterpret_cast<unsigned long long*>(ctl + 1);
+  uint8_t* d_status = reinterpret_cast<uint8_t*>(d_levels + levels_cap);
+  // frontier buffers (node, owner) x 2
+  unsigned long long cap = std::max<unsigned long long>(4ull * k, 1ull << 20);
+  if (const char* env = getenv("LFSR_PROBE_CAP"))  // testing: a tiny frontier forces the grow-and-redo path
+    cap = std::max<unsigned long long>(strtoull(env, nullptr, 10), k);  // (the roots always fit)
+  struct Pair {  // frees its buffers on every exit path
+    DevBuf b[2];
+    ~Pair() {
+      b[0].release();
+      b[1].release();
+    }
+  } fp;
+  DevBuf* fb = fp.b;
+  auto alloc = [&](DevBuf& b, unsigned long long c) { return b.ensure(c * 12); };
+  auto nodes_of = [&](DevBuf& b) { return b.as<uint64_t>(); };
+  auto owners_of = [&](DevBuf& b, unsigned long long c) { return reinterpret_cast<uint32_t*>(b.as<uint64_t>() + c); };
+  LC_CUDA(alloc(fb[0], cap));
+  LC_CUDA(alloc(fb[1], cap));
+  {  // level 0: the roots
+    std::vector<uint32_t> own(k);
+    for (uint64_t i = 0; i < k; ++i) own[i] = static_cast<uint32_t>(i);
+    LC_CUDA(cudaMemcpyAsync(nodes_of(fb[0]), roots, k * 8, cudaMemcpyHostToDevice, st));
+    LC_CUDA(cudaMemcpyAsync(owners_of(fb[0], cap), own.data(), k * 4, cudaMemcpyHostToDevice, st));
+    Ctl h{};
+    h.cnt[0] = k;
+    LC_CUDA(cudaMemcpyAsync(ctl, &h, sizeof h, cudaMemcpyHostToDevice, st));
+    LC_CUDA(cudaMemsetAsync(d_depth, 0, k * 8, st));
+    std::vector<uint64_t> ones(k, 1);
+    LC_CUDA(cudaMemcpyAsync(d_nodes, ones.data(), k * 8, cudaMemcpyHostToDevice, st));
+    LC_CUDA(cudaMemsetAsync(d_lvl, 0, k * 8, st));
+    LC_CUDA(cudaMemsetAsync(d_status, 0, k, st));
+    if (levels_cap) LC_CUDA(cudaMemsetAsync(d_levels, 0, static_cast<size_t>(levels_cap) * 8, st));
+    LC_CUDA(cudaStreamSynchronize(st));  // (host vectors go out of scope)
+  }
+  const int blocks = ctx->sms * 8;
+  uint64_t level = 0;
+  constexpr uint64_t kCheck = 16;  // levels between looks at the live count
+  for (;;) {
+    if (depth_cap >= 0 && level >= static_cast<uint64_t>(depth_cap)) {  // pipeline.py:280-281
+      LC_CUDA(lc::launch_probe_censor(kk, d_status, st));
+      g_launches += 1;
+      break;
+    }
+    const int a = static_cast<int>(level & 1), b = a ^ 1;
+    LC_CUDA(lc::launch_probe_expand(id, static_cast<uint32_t>(fixed_r3), nodes_of(fb[a]), owners_of(fb[a], cap),
+                                    &ctl->cnt[a], d_status, nodes_of(fb[b]), owners_of(fb[b], cap), &ctl->cnt[b], cap,
+                                    d_lvl, &ctl->overflow, blocks, st));
+    LC_CUDA(lc::launch_probe_finalize(kk, static_cast<uint32_t>(level), d_lvl, d_status, d_depth, d_nodes, d_levels,
+                                      levels_cap, node_cap, &ctl->overflow, &ctl->live[a], &ctl->done, &ctl->cnt[a],
+                                      &ctl->live[b], st));
+    g_launches += 2;
+    ++level;
+    if (level % kCheck != 0 && !(depth_cap >= 0 && level >= static_cast<uint64_t>(depth_cap))) continue;
+    Ctl h{};
+    LC_CUDA(cudaMemcpyAsync(&h, ctl, sizeof h, cudaMemcpyDeviceToHost, st));
+    LC_CUDA(cudaStreamSynchronize(st));
+    if (h.overflow) {  // level h.done did not fit: grow both buffers, keep its frontier, redo
+      const uint64_t redo = h.done;
+      const int ra = static_cast<int>(redo & 1), rb = ra ^ 1;
+      const unsigned long long need = h.cnt[rb];  // the attempted next-level size
+      const unsigned long long ncap = std::max<unsigned long long>(2 * cap, need + (need >> 2));
+      Pair np;
+      DevBuf* nb = np.b;
+      LC_CUDA(alloc(nb[0], ncap));
+      LC_CUDA(alloc(nb[1], ncap));
+      const unsigned long long cur = h.cnt[ra];
+      LC_CUDA(cudaMemcpyAsync(nodes_of(nb[ra]), nodes_of(fb[ra]), cur * 8, cudaMemcpyDeviceToDevice, st));
+      LC_CUDA(cudaMemcpyAsync(owners_of(nb[ra], ncap), owners_of(fb[ra], cap), cur * 4, cudaMemcpyDeviceToDevice,
+                              st));
+      LC_CUDA(cudaStreamSynchronize(st));
+      std::swap(fb[0], nb[0]);
+      std::swap(fb[1], nb[1]);
+      cap = ncap;
+      h.overflow = 0;
+      h.cnt[rb] = 0;
+      LC_CUDA(cudaMemcpyAsync(ctl, &h, sizeof h, cudaMemcpyHostToDevice, st));
+      LC_CUDA(cudaMemsetAsync(d_lvl, 0, k * 8, st));
+      LC_CUDA(cudaStreamSynchronize(st));
+      level = redo;
+      continue;
+    }
+    if (h.live[static_cast<int>((level - 1) & 1)] == 0) break;
+  }
+  LC_CUDA(cudaMemcpyAsync(depth, d_depth, k * 8, cudaMemcpyDeviceToHost, st));
+  LC_CUDA(cudaMemcpyAsync(nodes, d_nodes, k * 8, cudaMemcpyDeviceToHost, st));
+  LC_CUDA(cudaMemcpyAsync(censored, d_status, k, cudaMemcpyDeviceToHost, st));
+  if (levels_cap) LC_CUDA(cudaMemcpyAsync(level_counts, d_levels, static_cast<size_t>(levels_cap) * 8,
+                                          cudaMemcpyDeviceToHost, st));
+  LC_CUDA(cudaStreamSynchronize(st));
+  for (uint64_t i = 0; i < k; ++i) censored[i] = censored[i] == 2 ? 1 : 0;
+  if (levels_cap) level_counts[0] = k;
+  return LC_OK;
+}
+
 // ---------------------------------------------------------------- closure check
 
 int lc_first_missing(lc_ctx* ctx, const uint64_t* sorted_set, uint64_t m, const uint64_t* queries, uint64_t n,

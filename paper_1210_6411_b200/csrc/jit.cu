@@ -231,8 +231,9 @@ const CustomKernels* build_custom(const lc_spec* s, bool load, std::string* err)
        {&k->is_candidate, &k->predecessors, &k->clock, &k->enumerate}},
       {"prune.cu",
        {"&lc::prune2_kernel<" + S + ", " + ring + ", true>", "&lc::prune2_kernel<" + S + ", " + ring + ", false>",
-        "&lc::prune3_kernel<" + S + ", " + stack3 + ", true>", "&lc::prune3_kernel<" + S + ", " + stack3 + ", false>"},
-       {&k->prune_dfs, &k->prune_bfs, &k->prune3_dfs, &k->prune3_bfs}},
+        "&lc::prune3_kernel<" + S + ", " + stack3 + ", true>", "&lc::prune3_kernel<" + S + ", " + stack3 + ", false>",
+        "&lc::probe_expand_kernel<" + S + ">"},
+       {&k->prune_dfs, &k->prune_bfs, &k->prune3_dfs, &k->prune3_bfs, &k->probe_expand}},
   };
   for (Unit& u : units) {
     cudaLibrary_t lib;

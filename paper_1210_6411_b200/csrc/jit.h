@@ -17,7 +17,7 @@ struct CustomKernels {
   int clock_taps[3];
   cudaKernel_t walk_plain, walk_rearm, mode_probe;         // walk.cu (runtime F)
   cudaKernel_t is_candidate, predecessors, clock, enumerate;  // kernels.cu
-  cudaKernel_t prune_dfs, prune_bfs, prune3_dfs, prune3_bfs;  // prune.cu
+  cudaKernel_t prune_dfs, prune_bfs, prune3_dfs, prune3_bfs, probe_expand;  // prune.cu
 };
 
 // 0 if the spec is valid for the kernels (cipher.py:72-86 and a 64-bit state), else 1

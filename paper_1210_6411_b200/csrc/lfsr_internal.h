@@ -161,6 +161,19 @@ cudaError_t launch_prune3(SpecId id, uint32_t F, int mode, uint32_t limit, const
                           uint8_t* removed, uint64_t* work, unsigned long long* queue, void* spill, int blocks,
                           cudaStream_t stream);
 
+// Batched segment probes (prune.cu; pipeline.probe_segment): one expand launch and one
+// finalize launch per level, driven by lc_probe_segments.
+cudaError_t launch_probe_expand(SpecId id, uint32_t F, const uint64_t* fnode, const uint32_t* fowner,
+                                const unsigned long long* cur_count, const uint8_t* status, uint64_t* nnode,
+                                uint32_t* nowner, unsigned long long* next_count, unsigned long long cap,
+                                unsigned long long* lvl, unsigned int* overflow, int blocks, cudaStream_t st);
+cudaError_t launch_probe_finalize(uint32_t k, uint32_t level, unsigned long long* lvl, uint8_t* status,
+                                  uint64_t* depth, uint64_t* nodes, unsigned long long* level_counts,
+                                  uint32_t levels_cap, int64_t node_cap, const unsigned int* overflow,
+                                  unsigned long long* live, unsigned long long* done_count,
+                                  unsigned long long* cnt_reset, unsigned long long* live_reset, cudaStream_t st);
+cudaError_t launch_probe_censor(uint32_t k, uint8_t* status, cudaStream_t st);
+
 cudaError_t measure_lop3_peak(int sms, double* ops_per_s, double* sm_mhz);
 
 // Steps 4-5 (reduce.cu).  err_out: 0 ok, 1 unsorted sources, 2 not closed,

@@ -23,6 +23,7 @@
 // unsteps, cipher.py:221-225, and a select), so a warp's lanes diverge only over a few
 // predicated instructions.
 #ifndef __CUDACC_RTC__
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #endif
@@ -790,6 +791,110 @@ __global__ void __launch_bounds__(kThreads3) prune3_kernel(const uint64_t* __res
   }
 }
 
+// ------------------------------------------------------ batched segment probes
+// probe_segment (pipeline.py:262-298) for many roots at once, level-synchronous and
+// device-resident: one expand launch per level appends every live root's next level
+// (its frontier's children in the segment, `_expand`) to the other frontier buffer and
+// counts them per root; one finalize launch per root applies the reference's
+// bookkeeping for the level (depth, nodes, level_counts, the node cap).  The host only
+// launches (and looks at the live count every few levels); a frontier that would
+// overflow its buffer leaves the level uncommitted for the host to grow and redo.
+constexpr int kProbeThreads = 256;
+
+template <class S>
+__global__ void __launch_bounds__(kProbeThreads) probe_expand_kernel(
+    const uint64_t* __restrict__ fnode, const uint32_t* __restrict__ fowner, const unsigned long long* cur_count,
+    const uint8_t* __restrict__ status, uint32_t F, uint64_t* __restrict__ nnode, uint32_t* __restrict__ nowner,
+    unsigned long long* next_count, unsigned long long cap, unsigned long long* __restrict__ lvl,
+    unsigned int* overflow) {
+  __shared__ uint32_t tbl_words[16];
+  if (threadIdx.x < 16) tbl_words[threadIdx.x] = kChildTable.w[threadIdx.x];
+  __syncthreads();
+  if (*overflow) return;
+  const uint8_t* tbl = reinterpret_cast<const uint8_t*>(tbl_words);
+  const unsigned long long m = *cur_count;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kProbeThreads;
+  // warp-aligned loop: every lane of a warp runs the same iterations (warp-wide append)
+  for (uint64_t w0 = blockIdx.x * static_cast<uint64_t>(kProbeThreads) + (threadIdx.x & ~31u); w0 < m;
+       w0 += stride) {
+    const uint64_t i = w0 + lane;
+    uint32_t r1 = 0, r2 = 0, r3 = 0, mask = 0, o = 0;
+    if (i < m) {
+      o = fowner[i];
+      if (status[o] == 0) {
+        unpack2<S>(fnode[i], r1, r2, r3);
+        mask = child_set3<S>(tbl, r1, r2, r3, F);
+      }
+    }
+    const uint32_t c = __popc(mask);
+    uint32_t incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, d);
+      if (lane >= static_cast<uint32_t>(d)) incl += y;
+    }
+    const uint32_t tot = __shfl_sync(kFull, incl, 31);
+    unsigned long long base = 0;
+    if (lane == 31 && tot) base = atomicAdd(next_count, static_cast<unsigned long long>(tot));
+    base = __shfl_sync(kFull, base, 31) + (incl - c);
+    if (c) {
+      if (base + c > cap) {
+        atomicExch(overflow, 1u);
+      } else {
+        atomicAdd(&lvl[o], static_cast<unsigned long long>(c));
+        uint64_t k = base;
+        for (uint32_t q = 0; q < 4; ++q)  // LUT order, as the reference appends them
+          if ((mask >> q) & 1u) {
+            uint32_t c1 = r1, c2 = r2, c3 = r3;
+            child2<S>(c1, c2, c3, q);
+            nnode[k] = pack2<S>(c1, c2, c3);
+            nowner[k] = o;
+            ++k;
+          }
+      }
+    }
+  }
+}
+
+// status: 0 live, 1 done (empty level), 2 censored
+__global__ void probe_finalize_kernel(uint32_t k, uint32_t level, unsigned long long* __restrict__ lvl,
+                                      uint8_t* __restrict__ status, uint64_t* __restrict__ depth,
+                                      uint64_t* __restrict__ nodes, unsigned long long* __restrict__ level_counts,
+                                      uint32_t levels_cap, int64_t node_cap, const unsigned int* overflow,
+                                      unsigned long long* live, unsigned long long* done_count,
+                                      unsigned long long* cnt_reset, unsigned long long* live_reset) {
+  if (*overflow) return;
+  for (uint32_t o = blockIdx.x * blockDim.x + threadIdx.x; o < k; o += gridDim.x * blockDim.x) {
+    if (status[o] != 0) continue;
+    const unsigned long long c = lvl[o];
+    lvl[o] = 0;
+    if (c == 0) {  // pipeline.py:286-287: an empty next level ends the sweep
+      status[o] = 1;
+      continue;
+    }
+    depth[o] = level + 1;
+    nodes[o] += c;
+    if (level + 1 < levels_cap) atomicAdd(&level_counts[level + 1], c);
+    if (node_cap >= 0 && nodes[o] > static_cast<uint64_t>(node_cap)) {  // pipeline.py:293-294
+      status[o] = 2;
+      continue;
+    }
+    atomicAdd(live, 1ull);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    atomicAdd(done_count, 1ull);  // levels committed (the host redoes from here after an overflow)
+    cnt_reset[0] = 0;             // this level's frontier count: free for level + 2
+    live_reset[0] = 0;            // the next level's live count starts from zero
+  }
+}
+
+// pipeline.py:280-281: a sweep that reaches depth_cap is censored
+__global__ void probe_censor_kernel(uint32_t k, uint8_t* __restrict__ status) {
+  for (uint32_t o = blockIdx.x * blockDim.x + threadIdx.x; o < k; o += gridDim.x * blockDim.x)
+    if (status[o] == 0) status[o] = 2;
+}
+
 #ifndef LC_PRUNE2_RING
 #define LC_PRUNE2_RING 16
 #endif
@@ -863,6 +968,47 @@ int prune3_threads() { return kThreads3; }
 
 uint64_t prune3_spill_bytes(int blocks, uint32_t limit) {
   return static_cast<uint64_t>(blocks) * kThreads3 * limit * sizeof(uint4);
+}
+
+cudaError_t launch_probe_expand(SpecId id, uint32_t F, const uint64_t* fnode, const uint32_t* fowner,
+                                const unsigned long long* cur_count, const uint8_t* status, uint64_t* nnode,
+                                uint32_t* nowner, unsigned long long* next_count, unsigned long long cap,
+                                unsigned long long* lvl, unsigned int* overflow, int blocks, cudaStream_t st) {
+  switch (id) {
+#define LC_PROBE_LAUNCH(SP)                                                                                        \
+  probe_expand_kernel<SP><<<blocks, kProbeThreads, 0, st>>>(fnode, fowner, cur_count, status, F, nnode, nowner, \
+                                                            next_count, cap, lvl, overflow);                     \
+  break;
+    case SpecId::A51: LC_PROBE_LAUNCH(A51)
+    case SpecId::MINI567: LC_PROBE_LAUNCH(MINI567)
+    case SpecId::MINI789: LC_PROBE_LAUNCH(MINI789)
+#undef LC_PROBE_LAUNCH
+    case SpecId::CUSTOM: {
+      const CustomKernels* c = current_custom();
+      if (!c) return cudaErrorInvalidValue;
+      return jit_launch(c->probe_expand, blocks, kProbeThreads, 0, st, fnode, fowner, cur_count, status, F, nnode,
+                        nowner, next_count, cap, lvl, overflow);
+    }
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_probe_finalize(uint32_t k, uint32_t level, unsigned long long* lvl, uint8_t* status,
+                                  uint64_t* depth, uint64_t* nodes, unsigned long long* level_counts,
+                                  uint32_t levels_cap, int64_t node_cap, const unsigned int* overflow,
+                                  unsigned long long* live, unsigned long long* done_count,
+                                  unsigned long long* cnt_reset, unsigned long long* live_reset, cudaStream_t st) {
+  const unsigned g = static_cast<unsigned>(std::min<uint64_t>((k + 255) / 256, 1024));
+  probe_finalize_kernel<<<g ? g : 1, 256, 0, st>>>(k, level, lvl, status, depth, nodes, level_counts, levels_cap,
+                                                  node_cap, overflow, live, done_count, cnt_reset, live_reset);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_probe_censor(uint32_t k, uint8_t* status, cudaStream_t st) {
+  const unsigned g = static_cast<unsigned>(std::min<uint64_t>((k + 255) / 256, 1024));
+  probe_censor_kernel<<<g ? g : 1, 256, 0, st>>>(k, status);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_prune3(SpecId id, uint32_t F, int mode, uint32_t limit, const uint64_t* cands, uint64_t n,

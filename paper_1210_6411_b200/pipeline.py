@@ -210,52 +210,35 @@ def build_skeleton_edges(skeleton: list, params: CandidateParams, spec: CipherSp
 
 def probe_segments(roots, spec: CipherSpec, params: CandidateParams, *, depth_cap: int | None = None,
                    node_cap: int | None = None, level_counts: list | None = None):
-    """Batched probe_segment: per root (depth, nodes, censored) arrays.  Each level of
-    every live segment is expanded in one GPU predecessor + predicate pass."""
-    roots = np.asarray(roots, dtype=np.uint64).reshape(-1)
+    """Batched probe_segment (pipeline.py:262-298): per root (depth, nodes, censored)
+    arrays.  The sweeps run device-resident (lc_probe_segments: one expand and one
+    finalize launch per level for all roots); ``level_counts`` accumulates nodes per
+    depth level summed over the roots (index 0 counts the roots)."""
+    roots = np.ascontiguousarray(np.asarray(roots, dtype=np.uint64).reshape(-1))
     k = roots.size
-    depth = np.zeros(k, dtype=np.int64)
-    nodes = np.ones(k, dtype=np.int64)
-    censored = np.zeros(k, dtype=bool)
-    live = np.ones(k, dtype=bool)
+    depth = np.zeros(k, dtype=np.uint64)
+    nodes = np.ones(k, dtype=np.uint64)
+    censored = np.zeros(k, dtype=np.uint8)
+    if k == 0:
+        return depth.astype(np.int64), nodes.astype(np.int64), censored.astype(bool)
+    cap_levels = (int(depth_cap) + 1) if depth_cap is not None else 1 << 20
+    cap_levels = max(1, min(cap_levels, 1 << 24))
+    levels = np.zeros(cap_levels, dtype=np.uint64)
+    ctx = N.context()
+    N.check(N.lib.lc_probe_segments(ctx.handle, C.byref(N.spec_struct(spec)), params.fixed_r3, N.u64p(roots), k,
+                                    -1 if depth_cap is None else int(depth_cap),
+                                    -1 if node_cap is None else int(node_cap), N.u64p(depth), N.u64p(nodes),
+                                    censored.ctypes.data_as(C.POINTER(C.c_uint8)), N.u64p(levels), cap_levels))
+    depth = depth.astype(np.int64)
     if level_counts is not None:
-        if not level_counts:
+        top = int(depth.max()) + 1
+        if top > cap_levels:
+            raise ValueError("segment deeper than the level-count buffer (pass a depth_cap)")
+        while len(level_counts) < top:
             level_counts.append(0)
-        level_counts[0] += k
-    front, owner = roots.copy(), np.arange(k)
-    level = 0
-    while live.any():
-        if depth_cap is not None and level >= depth_cap:
-            censored[live] = True
-            break
-        preds, cnt = _batch.predecessors(front, spec)
-        sel = np.arange(4)[None, :] < cnt[:, None]
-        cand_nodes = preds[sel]
-        cand_owner = np.repeat(owner, cnt.astype(np.int64))
-        on_plane = (cand_nodes & np.uint64(params.r3_field_mask)) == np.uint64(params.packed_r3)
-        drop = np.zeros(cand_nodes.size, dtype=bool)
-        if on_plane.any():
-            drop[on_plane] = _batch.is_candidate(cand_nodes[on_plane], params, spec)
-        nxt, nowner = cand_nodes[~drop], cand_owner[~drop]
-        per = np.bincount(nowner, minlength=k)
-        finished = live & (per == 0)
-        live &= ~finished
-        if not live.any():
-            break
-        level += 1
-        depth[live] = level
-        nodes[live] += per[live]
-        if level_counts is not None:
-            if len(level_counts) <= level:
-                level_counts.append(0)
-            level_counts[level] += int(per[live].sum())
-        if node_cap is not None:
-            over = live & (nodes > node_cap)
-            censored |= over
-            live &= ~over
-        keep = live[nowner]
-        front, owner = nxt[keep], nowner[keep]
-    return depth, nodes, censored
+        for lv in range(top):
+            level_counts[lv] += int(levels[lv])
+    return depth, nodes.astype(np.int64), censored.astype(bool)
 
 
 def probe_segment(root: int, spec: CipherSpec, params: CandidateParams,

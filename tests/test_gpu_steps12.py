@@ -106,6 +106,35 @@ def test_probe_segment_minis(gpu, lc, specs, params, name):
         assert lc_ == levels
 
 
+@pytest.mark.parametrize("frontier", [None, "64"])
+def test_probe_segments_batched_match_oracle(gpu, lc, specs, params, frontier, monkeypatch):
+    """Batched device-resident probes (lc_probe_segments) equal the C restatement root by
+    root -- depth, nodes, censoring, and the level counts summed over the roots -- with and
+    without caps; LFSR_PROBE_CAP=64 starts the frontier buffers tiny, so every few levels
+    overflow and are grown and redone."""
+    from oracle import port
+
+    if frontier:
+        monkeypatch.setenv("LFSR_PROBE_CAP", frontier)
+    for name, n_roots, caps in (("mini567", 200, [(None, None), (5, None), (None, 40)]),
+                                ("mini789", 300, [(None, None), (12, 500)]),
+                                ("a51", 256, [(3000, 200000), (400, None)])):
+        roots = lc.random_candidates_gpu(specs[name], params[name], seed=31, n=n_roots)
+        for depth_cap, node_cap in caps:
+            levels = []
+            d, nn, c = lc.pipeline.probe_segments(roots, specs[name], params[name], depth_cap=depth_cap,
+                                                  node_cap=node_cap, level_counts=levels)
+            want_levels = []
+            for i, x in enumerate(roots):
+                wd, wn, wc, wl = port.probe_segment(specs[name], params[name].fixed_r3, int(x), depth_cap, node_cap,
+                                                    levels=8192)
+                assert (int(d[i]), int(nn[i]), bool(c[i])) == (wd, wn, wc), (name, depth_cap, node_cap, i)
+                want_levels += [0] * (len(wl) - len(want_levels))
+                for lv, v in enumerate(wl):
+                    want_levels[lv] += int(v)
+            assert levels == want_levels, (name, depth_cap, node_cap)
+
+
 @pytest.mark.parametrize("name", ["mini567", "mini789"])
 def test_build_skeleton_edges_closed_set(gpu, lc, specs, params, name):
     g = golden_npz(f"edges_{name}")
