@@ -752,6 +752,7 @@ int lc_prune_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int32_t
   // (testing: small values exercise the drop-and-climb fallback)
   uint32_t spill_cap = LC_PRUNE_SPILL;
   if (const char* env = getenv("LFSR_PRUNE_SPILL")) spill_cap = static_cast<uint32_t>(strtoul(env, nullptr, 10));
+  int prune3_blocks = 0;
   const char* v1 = getenv("LFSR_PRUNE_V1");  // A/B: the round-1 kernel (64-bit node, no register cache)
   if (v1 && v1[0] == '1' && id != lc::SpecId::CUSTOM) {
     const int ring = lc::prune_ring_for(n);
@@ -760,18 +761,25 @@ int lc_prune_device(lc_ctx* ctx, const lc_spec* spec, uint64_t fixed_r3, int32_t
     LC_CUDA(lc::launch_prune(id, static_cast<uint32_t>(fixed_r3), mode, limit, d_cands, n, d_removed, d_work,
                              ctx->pq.as<unsigned long long>(), spill_cap ? ctx->spill.p : nullptr, spill_cap, ring,
                              blocks, st));
-  } else if (limit <= lc::prune3_max_limit() && !(v1 && v1[0] == '2')) {
-    // the uniform-step kernel (LFSR_PRUNE_V1=2 selects the v2 kernel for A/B); a stack
-    // holds at most `limit` entries in either mode (DFS: ancestors at distinct depths <=
-    // limit; BFS: the traversal stops past `limit` nodes); the grid is capped by the
-    // batch so small batches do not allocate every lane's stack
-    const uint64_t lanes_max = (n + 31) / 32 * 32;
-    int blocks = lc::prune3_blocks_per_sm(id) * ctx->sms;
-    const uint64_t need_blocks = (lanes_max + lc::prune3_threads() - 1) / lc::prune3_threads();
-    if (static_cast<uint64_t>(blocks) > need_blocks) blocks = static_cast<int>(need_blocks);
-    LC_CUDA(ctx->spill.ensure(lc::prune3_spill_bytes(blocks, static_cast<uint32_t>(limit))));
+  } else if (limit <= lc::prune3_max_limit() && !(v1 && v1[0] == '2') &&
+             [&] {  // the uniform-step kernel, if its stacks fit in device memory
+               // (LFSR_PRUNE_V1=2 selects the v2 kernel for A/B).  A stack holds at most
+               // `limit` entries in either mode (DFS: ancestors at distinct depths <=
+               // limit; BFS: the traversal stops past `limit` nodes); the grid is capped
+               // by the batch so small batches do not allocate every lane's stack.
+               const uint64_t lanes_max = (n + 31) / 32 * 32;
+               int blocks = lc::prune3_blocks_per_sm(id) * ctx->sms;
+               const uint64_t need_blocks = (lanes_max + lc::prune3_threads() - 1) / lc::prune3_threads();
+               if (static_cast<uint64_t>(blocks) > need_blocks) blocks = static_cast<int>(need_blocks);
+               if (ctx->spill.ensure(lc::prune3_spill_bytes(blocks, static_cast<uint32_t>(limit))) != cudaSuccess) {
+                 cudaGetLastError();  // out of memory: fall through to v2 (bounded spill rings)
+                 return false;
+               }
+               prune3_blocks = blocks;
+               return true;
+             }()) {
     LC_CUDA(lc::launch_prune3(id, static_cast<uint32_t>(fixed_r3), mode, static_cast<uint32_t>(limit), d_cands, n,
-                              d_removed, d_work, ctx->pq.as<unsigned long long>(), ctx->spill.p, blocks, st));
+                              d_removed, d_work, ctx->pq.as<unsigned long long>(), ctx->spill.p, prune3_blocks, st));
   } else {
     const int blocks = lc::prune2_blocks_per_sm(id, mode) * ctx->sms;
     if (spill_cap) LC_CUDA(ctx->spill.ensure(lc::prune2_spill_bytes(blocks, spill_cap)));
