@@ -740,6 +740,7 @@ __global__ void __launch_bounds__(kThreads3) prune3_kernel(const uint64_t* __res
         }
         if (sp == lo) {  // not cached (no room was left to prefetch it): fetch it now
           lo -= kChunk3;  // lo stays a multiple of the chunk: its slots are consecutive
+          LC_CHECK(lo % kChunk3 == 0 && lo + kChunk3 <= sp && sp <= gcap);
           const uint32_t s0 = ring_s + (lo & (K - 1)) * kSlot;
 #pragma unroll
           for (int j = 0; j < kChunk3; ++j) cp_async16(s0 + j * kSlot, my + lo + j);
@@ -777,6 +778,7 @@ __global__ void __launch_bounds__(kThreads3) prune3_kernel(const uint64_t* __res
         if (pfhi) cp_async_wait_all();
         pfhi = lo;
         lo -= kChunk3;
+        LC_CHECK(lo % kChunk3 == 0 && sp - lo <= static_cast<uint32_t>(K) && sp <= gcap);
         const uint32_t s0 = ring_s + (lo & (K - 1)) * kSlot;
 #pragma unroll
         for (int j = 0; j < kChunk3; ++j) cp_async16(s0 + j * kSlot, my + lo + j);
