@@ -454,7 +454,7 @@ def main() -> None:
         import bench_steps12
 
         torch.cuda.empty_cache()
-        steps12 = bench_steps12.measure(ctx, stream, prune_log2=26, cpu_sample=1 << 16,
+        steps12 = bench_steps12.measure(ctx, stream, prune_log2=27, cpu_sample=1 << 16,
                                         lop3_peak=(lop3_peak, peak_mhz))
 
     if rank == 0:

@@ -159,7 +159,11 @@ def measure(ctx, stream, *, rows_log2: int = 13, prune_log2: int = 26, depth: in
                                       C.c_void_p(cands.data_ptr()), npr, C.c_void_p(removed.data_ptr()),
                                       C.c_void_p(work.data_ptr()), C.c_void_p(stream.cuda_stream)))
 
+    # warm-up on a 2^20 prefix (same grid and stack allocation as the timed launch)
+    npr_full = npr
+    npr = min(npr_full, 1 << 20)
     prune()
+    npr = npr_full
     torch.cuda.synchronize()
     e0.record(stream)
     prune()
