@@ -28,5 +28,6 @@ from .reduce import (CycleRecord, IterationLog, NotAPermutationError, PassStats,
 from .ground_truth import CycleInfo, GroundTruth, brute_force_analysis  # noqa: F401
 from .stats import (AnalysisReport, ExpectationTable, SampleStats, deviation_report,  # noqa: F401
                     random_mapping_expectations, sample_segment_distances, sample_segment_shapes)
+from .step3 import merge_edge_files, walk_to_edge_files  # noqa: F401
 
 __version__ = "0.1.0"
