@@ -77,3 +77,39 @@ def test_minimal_walk_sort_and_generator_inputs(gpu, lc, specs, params):
     assert [int(c[0]) for c in s1] == [7, 7, 1]
     assert _batch.first_missing(np.zeros(0, dtype=np.uint64), np.array([5], dtype=np.uint64)) == 0
     assert _batch.first_missing(np.array([5], dtype=np.uint64), np.zeros(0, dtype=np.uint64)) == 0
+
+
+@pytest.mark.parametrize("kernel", ["v3", "v2"])
+def test_prune_partial_warps_match_oracle(gpu, lc, specs, params, kernel, monkeypatch):
+    """Batches smaller than a warp, a warp plus one, and one lane short of a block: the
+    prune's per-lane candidate tickets, the drained-queue exit and (v3) the grid sized to
+    the batch, in both modes; results equal the C restatement."""
+    from oracle import port
+    from paper_1210_6411_b200 import _batch
+
+    if kernel == "v2":
+        monkeypatch.setenv("LFSR_PRUNE_V1", "2")
+    for name in ("a51", "mini789"):
+        pool = lc.random_candidates_gpu(specs[name], params[name], seed=123, n=300)
+        for n in (1, 2, 31, 33, 127, 129, 300):
+            cands = pool[:n]
+            for mode, limit in (("dfs", 3000 if name == "a51" else 60), ("bfs", 500)):
+                removed, work = _batch.prune(cands, specs[name], params[name], mode, limit)
+                o_removed, o_work = port.prune(specs[name], params[name].fixed_r3, mode, limit, cands)
+                assert (removed == np.asarray(o_removed).astype(bool)).all(), (name, n, mode)
+                assert (work == np.asarray(o_work)).all(), (name, n, mode)
+
+
+def test_probe_segments_tiny_batches(gpu, lc, specs, params):
+    """Zero and one root through the device-resident probe, with and without caps."""
+    from oracle import port
+
+    d, nn, c = lc.pipeline.probe_segments([], specs["mini567"], params["mini567"])
+    assert d.size == 0 and nn.size == 0 and c.size == 0
+    root = int(lc.random_candidates_gpu(specs["a51"], params["a51"], seed=4, n=1)[0])
+    for depth_cap, node_cap in ((None, None), (3, None), (None, 10)):
+        lv = []
+        got = lc.probe_segment(root, specs["a51"], params["a51"], depth_cap=depth_cap, node_cap=node_cap,
+                               level_counts=lv)
+        wd, wn, wc, wl = port.probe_segment(specs["a51"], 0x2AAA00, root, depth_cap, node_cap)
+        assert got == (wd, wn, wc) and lv == [int(v) for v in wl]
