@@ -7,8 +7,10 @@ resident, out of place.
 Prints one JSON line per size: time per sort, records/s, and the HBM roofline of the
 whole sort.  Algorithmic bytes per record: histogram + payload pack 72 (key and four
 payload columns read, the 32-byte record-major payload written); the first pass 20 (key
-in; key + row out); each middle pass 24 (key + row in and out); the last pass 84 (key +
-row in, the record's 32-byte payload, five output columns).  L2 is flushed before every
+in; key + row out); each further pass 24 (key + row in and out); the LSD route's last
+pass 84 (key + row in, the record's 32-byte payload, five output columns); the MSD route
+(from 2^16 records) adds the window histogram (8) and the group bounds (8) and ends with
+the per-group sort (84, like the LSD last pass).  L2 is flushed before every
 timed sort.  Parity: the output equals numpy's stable argsort order
 (checked at the smallest size).
 """
@@ -84,9 +86,21 @@ def main():
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
         s = min(times)
-        alg = n * (72 + 20 + 24 * (varying_bytes - 2) + 84)
+        # algorithmic bytes of the route the device picks (csrc/sort.cu): LSD below 2^16
+        # records -- 72 (histogram + payload pack) + 20 (first pass) + 24 per further pass
+        # + 84 (last pass, payload gather) -- else MSD: 72 + 8 (window histogram) + 20 + 24
+        # per further window pass + 8 (group bounds) + 84 (per-group sort: key + row in,
+        # key out, payload gathered and written)
+        lg = (n - 1).bit_length()
+        W = min(max(lg - 10, 8), 22) if n >= 1 << 16 else 0
+        if W:
+            nd = (W + 7) // 8
+            alg = n * (72 + 8 + 20 + 24 * (nd - 1) + 8 + 84)
+        else:
+            alg = n * (72 + 20 + 24 * (varying_bytes - 2) + 84)
         line = {"metric": "edge-output sort (5-column records by source)", "records": n, "keys": args.keys,
-                "passes_run": varying_bytes, "seconds": s, "records_per_s": n / s,
+                "route": f"msd (window {W} bits)" if W else f"lsd ({varying_bytes} passes)",
+                "seconds": s, "records_per_s": n / s,
                 "roofline": {"bound": "hbm", "achieved": alg / s / 1e9, "peak": hbm / 1e9 if hbm else None,
                              "unit": "GB/s", "frac": alg / s / hbm if hbm else None,
                              "algorithmic_bytes_per_record": alg / n,

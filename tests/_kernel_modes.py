@@ -80,9 +80,10 @@ def main(mode: str) -> None:
         assert (rem == o_rem).all() and (work == o_work).all()
     elif mode == "sort":
         rng = np.random.default_rng(4)
-        for n in (4097, 300_000):
+        for n, dups in ((4097, True), (300_000, True), (300_000, False)):
             src = rng.integers(0, 1 << 63, size=n, dtype=np.uint64)
-            src[::7] = src[0]  # duplicates: the sort must be stable
+            if dups:  # duplicates: the sort must be stable (and at 300k one group outgrows
+                src[::7] = src[0]  # the MSD route's shared-memory sort: the LSD fallback)
             dst = np.arange(n, dtype=np.uint64)
             s, d, _ = lc.sort_edge_arrays(src, dst, dst.copy())
             order = np.argsort(src, kind="stable")

@@ -3,7 +3,8 @@ ascending by source (records.py:3-5, reduce.py:3-4), stable like numpy's argsort
 "stable"), through the host API (reduce.sort_edge_arrays -> lc_sort_edges) and the
 asynchronous device API (lc_sort_edges_device).  Key shapes: full 64-bit random, A5/1
 skeleton sources (constant R3 bytes -> skipped passes), already ascending (no pass runs),
-heavy duplicates, descending, tile-boundary sizes."""
+heavy duplicates, descending, tile-boundary sizes; from 2^16 records the MSD route (bit
+windows + per-group shared-memory sorts) with its LSD fallback for oversized groups."""
 
 from __future__ import annotations
 
@@ -30,11 +31,15 @@ def _keys(kind, n, rng):
         return rng.integers(0, 37, size=n, dtype=np.uint64) << np.uint64(23)
     if kind == "constant":
         return np.full(n, 0x1234_5678_9ABC_DEF0, dtype=np.uint64)
+    if kind == "clustered":  # few distinct high parts, random low bits: groups too big for the
+        # MSD route's per-group shared-memory sort -> the device falls back to the LSD passes
+        return (rng.integers(0, 37, size=n, dtype=np.uint64) << np.uint64(40)) | \
+            rng.integers(0, 1 << 30, size=n, dtype=np.uint64)
     raise ValueError(kind)
 
 
-@pytest.mark.parametrize("kind", ["random64", "a51", "sorted", "descending", "dups", "constant"])
-@pytest.mark.parametrize("n", [1, 2, 4095, 4096, 4097, 300_001])
+@pytest.mark.parametrize("kind", ["random64", "a51", "sorted", "descending", "dups", "constant", "clustered"])
+@pytest.mark.parametrize("n", [1, 2, 4095, 4096, 4097, 65_537, 300_001])
 def test_host_sort_is_stable_argsort(gpu, lc, kind, n):
     rng = np.random.default_rng(n * 7 + len(kind))
     src = _keys(kind, n, rng)
