@@ -544,6 +544,7 @@ __global__ void __launch_bounds__(kLocalThreads, LC_SORT_LOCAL_MINBLOCKS) msd_lo
     uint32_t* wh = whist + w * kLocalStride;
 #pragma unroll
     for (int k = 0; k < kLocalItems; ++k) {  // in input order within the warp: stable
+      if (wbase + k * 32 >= size) break;     // (warp-uniform: the warp's records are done)
       const uint32_t j = wbase + k * 32 + lane;
       const uint32_t d = j < size ? static_cast<uint32_t>(key[k] >> shift) & dmask : static_cast<uint32_t>(kLocalBins);
       const uint32_t peers = peers_of10(d);
