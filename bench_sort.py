@@ -92,7 +92,7 @@ def main():
         # per further window pass + 8 (group bounds) + 84 (per-group sort: key + row in,
         # key out, payload gathered and written)
         lg = (n - 1).bit_length()
-        W = min(max(lg - 10, 8), 22) if n >= 1 << 16 else 0
+        W = min(max(lg - 10, 8), 22) if n >= 1 << 16 and os.environ.get("LFSR_SORT_LSD") != "1" else 0
         if W:
             nd = (W + 7) // 8
             alg = n * (72 + 8 + 20 + 24 * (nd - 1) + 8 + 84)

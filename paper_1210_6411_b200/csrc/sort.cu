@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "lfsr_internal.h"
 
@@ -696,7 +697,9 @@ cudaError_t radix_sort_records(uint64_t n, const uint64_t* const* cols_in, uint6
   if (n >= (1ull << 32) || ncols < 1 || ncols > kCols) return cudaErrorInvalidValue;
   if (scratch_bytes < radix_sort_scratch_bytes(n)) return cudaErrorInvalidValue;
   if (n == 0) return cudaSuccess;
-  const uint32_t W = msd_window_bits(n);
+  // LFSR_SORT_LSD=1 forces the LSD route (A/B, tests)
+  const char* lsd_only = getenv("LFSR_SORT_LSD");
+  const uint32_t W = lsd_only && lsd_only[0] == '1' ? 0u : msd_window_bits(n);
   const uint64_t groups = W ? (1ull << W) : 1ull;
   uint8_t* p = static_cast<uint8_t*>(scratch);
   SortCtl* ctl = reinterpret_cast<SortCtl*>(p);

@@ -38,9 +38,14 @@ def _keys(kind, n, rng):
     raise ValueError(kind)
 
 
+@pytest.mark.parametrize("route", ["auto", "lsd"])
 @pytest.mark.parametrize("kind", ["random64", "a51", "sorted", "descending", "dups", "constant", "clustered"])
 @pytest.mark.parametrize("n", [1, 2, 4095, 4096, 4097, 65_537, 300_001])
-def test_host_sort_is_stable_argsort(gpu, lc, kind, n):
+def test_host_sort_is_stable_argsort(gpu, lc, kind, n, route, monkeypatch):
+    if route == "lsd":
+        if n < 65_537:
+            pytest.skip("below 2^16 records the LSD route is the only one")
+        monkeypatch.setenv("LFSR_SORT_LSD", "1")  # the LSD route at sizes that default to MSD
     rng = np.random.default_rng(n * 7 + len(kind))
     src = _keys(kind, n, rng)
     dst = rng.integers(0, 1 << 62, size=n, dtype=np.uint64)
