@@ -322,3 +322,25 @@ def test_prune_random_configs_match_restatement(gpu, lc, specs, params, kernel, 
         o_removed, o_work = port.prune(specs[name], params[name].fixed_r3, mode, limit, cands)
         assert (removed == np.asarray(o_removed).astype(bool)).all(), (name, mode, limit)
         assert (work == np.asarray(o_work)).all(), (name, mode, limit)
+
+
+@pytest.mark.parametrize("fixed_r3", [0x7FFC00, 0x123C00, 0x2AA800, 0x2A8000])
+@pytest.mark.parametrize("kernel", ["v3", "v2"])
+def test_prune_other_fixed_r3_matches_oracle(gpu, lc, specs, fixed_r3, kernel, monkeypatch):
+    """Fixed-R3 planes other than the paper's 0x2AAA00, one per (clock bit, bit above) class
+    that has candidates (c3 = 1, n3 = 0 planes have none; the prune kernels take F at run
+    time: the special-child test depends on it): candidates of the plane, DFS and BFS,
+    against the C restatement."""
+    from oracle import port
+    from paper_1210_6411_b200 import _batch
+
+    if kernel == "v2":
+        monkeypatch.setenv("LFSR_PRUNE_V1", "2")
+    p = lc.CandidateParams.from_spec(specs["a51"], fixed_r3)
+    cands = lc.enumerate_candidates_array(specs["a51"], p, 0x2AAA, 0x2AAB)[:3000]
+    assert cands.size and (cands == port.enumerate_rows(specs["a51"], fixed_r3, 0x2AAA, 0x2AAB)[:3000]).all()
+    for mode, limit in (("dfs", 3000), ("dfs", 40), ("bfs", 700)):
+        removed, work = _batch.prune(cands, specs["a51"], p, mode, limit)
+        o_removed, o_work = port.prune(specs["a51"], fixed_r3, mode, limit, cands)
+        assert (removed == np.asarray(o_removed).astype(bool)).all(), (mode, limit)
+        assert (work == np.asarray(o_work)).all(), (mode, limit)
