@@ -217,6 +217,7 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-steps12", action="store_true")
+    ap.add_argument("--no-next", action="store_true")  # skip the §8(f) sort / leaf-cut object
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
 
@@ -456,6 +457,12 @@ def main() -> None:
         torch.cuda.empty_cache()
         steps12 = bench_steps12.measure(ctx, stream, prune_log2=27, cpu_sample=1 << 16,
                                         lop3_peak=(lop3_peak, peak_mhz))
+    next_rows = None
+    if rank == 0 and world == 1 and not args.no_next:
+        import bench_reduce
+
+        torch.cuda.empty_cache()
+        next_rows = bench_reduce.measure_next()
 
     if rank == 0:
         clk = clocks.summary()
@@ -516,6 +523,7 @@ def main() -> None:
             "e2e": e2e,
             "cpu_baseline": cpu,
             "steps12": steps12,
+            "next_rows": next_rows,
         }
         print(json.dumps(line), flush=True)
     if multi:

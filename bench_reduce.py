@@ -102,5 +102,107 @@ def main():
     print(json.dumps(line), flush=True)
 
 
+def measure_next(sort_log2: int = 26, cut_log2: int = 24) -> dict:
+    """The §8(f) rows for the default bench line (bench.py): the edge-output sort of a
+    device-resident 5-column record set (A5/1 skeleton sources) with its HBM roofline,
+    and device-resident leaf cutting to the fixpoint on a seeded random mapping; parity of
+    sort + cut + cycle count against oracle/reduce_np.py on a 2^20 instance."""
+    import ctypes as C
+
+    import torch
+
+    import paper_1210_6411_b200 as lc
+    from oracle import reduce_np
+    from paper_1210_6411_b200 import _native as N
+    from paper_1210_6411_b200.reduce import cut_leaves_tensors
+
+    def instance(k, seed):
+        rng = np.random.default_rng(seed)
+        n = 1 << k
+        src = np.unique(rng.integers(0, 1 << 62, size=n + n // 64, dtype=np.uint64))[:n]
+        rng.shuffle(src)
+        dst = src[rng.integers(0, n, size=n)]
+        dist = rng.integers(11_000_000, 11_400_000, size=n, dtype=np.uint64)
+        return src, dst, dist
+
+    s, d, w = instance(20, 1)
+    s, d, w = lc.sort_edge_arrays(s, d, w)
+    z = np.zeros(s.size, dtype=np.uint64)
+    got = lc.cut_leaves_arrays(s, d, w, z, z)
+    want = reduce_np.cut_leaves(s, d, w, z, z)
+    parity = got[5] == want[5] and all((a == b).all() for a, b in zip(got[:5], want[:5]))
+    cyc = lc.count_cycles_arrays(*got[:4])
+    parity = bool(parity and [tuple(r) for r in zip(*(c.tolist() for c in cyc))] == reduce_np.count_cycles(*want[:4]))
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ctx = N.context(dev.index)
+    st = torch.cuda.current_stream(dev)
+    n = 1 << sort_log2
+    g = torch.Generator(device=dev)
+    g.manual_seed(sort_log2)
+    r1 = torch.randint(1, 1 << 19, (n,), device=dev, generator=g)
+    r2 = torch.randint(1, 1 << 22, (n,), device=dev, generator=g)
+    cols = [r1 | (r2 << 19) | (0x2AAA00 << 41), torch.randint(0, 1 << 62, (n,), device=dev, generator=g),
+            torch.arange(n, device=dev), torch.zeros(n, dtype=torch.int64, device=dev),
+            torch.zeros(n, dtype=torch.int64, device=dev)]
+    del r1, r2
+    outs = [torch.empty_like(c) for c in cols]
+    pin = (C.c_void_p * 5)(*[c.data_ptr() for c in cols])
+    pout = (C.c_void_p * 5)(*[c.data_ptr() for c in outs])
+
+    def run():
+        N.check(N.lib.lc_sort_edges_device(ctx.handle, n, pin, pout, C.c_void_p(st.cuda_stream)))
+
+    run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    run()
+    e1.record(st)
+    torch.cuda.synchronize()
+    sort_s = e0.elapsed_time(e1) / 1e3
+    ascending = bool((outs[0][1:] >= outs[0][:-1]).all().item())
+    # stable: rows (the arange column) ascend within equal sources
+    eq = outs[0][1:] == outs[0][:-1]
+    stable = bool(((outs[2][1:] > outs[2][:-1]) | ~eq).all().item())
+    W = min(max((n - 1).bit_length() - 10, 8), 22)
+    alg = n * (72 + 8 + 20 + 24 * ((W + 7) // 8 - 1) + 8 + 84)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 0.0)) * 1e9 or None
+    del cols, outs
+    torch.cuda.empty_cache()
+
+    src, dst, dist = instance(cut_log2, 2)
+    src, dst, dist = lc.sort_edge_arrays(src, dst, dist)
+    zc = np.zeros(src.size, dtype=np.uint64)
+    tens = [torch.from_numpy(c.view(np.int64)).to(dev) for c in (src, dst, dist, zc, zc)]
+    torch.cuda.synchronize()
+    e0.record(st)
+    n_out, passes = cut_leaves_tensors(*tens)
+    e1.record(st)
+    torch.cuda.synchronize()
+    cut_s = e0.elapsed_time(e1) / 1e3
+    del tens
+    return {
+        "edge_sort": {"workload": f"2^{sort_log2} device-resident 5-column records, A5/1 skeleton-like sources",
+                      "records": n, "seconds": sort_s, "records_per_s": n / sort_s,
+                      "route": f"msd (window {W} bits)", "ascending": ascending, "stable": stable,
+                      "roofline": {"bound": "hbm", "achieved": alg / sort_s / 1e9,
+                                   "peak": hbm / 1e9 if hbm else None, "unit": "GB/s",
+                                   "frac": alg / sort_s / hbm if hbm else None,
+                                   "algorithmic_bytes_per_record": alg / n,
+                                   "peak_source": "MEASURED_PEAKS.json hbm_gbs"}},
+        "leaf_cut": {"workload": f"seeded random mapping on 2^{cut_log2} sources, device-resident",
+                     "records": int(src.size), "seconds": cut_s, "records_per_s": src.size / cut_s,
+                     "passes": len(passes), "fixpoint_records": int(n_out)},
+        "parity_2p20_sort_cut_cycles_vs_restatement": parity,
+    }
+
+
 if __name__ == "__main__":
     main()

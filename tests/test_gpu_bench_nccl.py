@@ -36,7 +36,7 @@ def test_one_rank_nccl_bench(gpu, lc, specs, params):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(ROOT, "bench.py"),
            "--gpus", "1", "--steps", "2", "--warmup", "3", "--workload-log2", str(log2), "--batch-log2", str(log2 - 1),
-           "--no-cpu", "--no-steps12"]
+           "--no-cpu", "--no-steps12", "--no-next"]
     out = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
     line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
