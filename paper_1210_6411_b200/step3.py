@@ -96,6 +96,20 @@ def read_manifest(out_dir: str, rank: int = 0):
     return cfg, done
 
 
+def _fsync_dir(path: str) -> None:
+    """Make a rename in ``path`` durable (POSIX: the directory entry lives in the directory)."""
+    try:
+        fd = os.open(path, os.O_RDONLY)
+    except OSError:
+        return
+    try:
+        os.fsync(fd)
+    except OSError:
+        pass
+    finally:
+        os.close(fd)
+
+
 def _append(path: str, obj: dict) -> None:
     with open(path, "a") as f:
         f.write(json.dumps(obj) + "\n")
@@ -147,6 +161,7 @@ def walk_to_edge_files(states, out_dir: str, spec: CipherSpec, params: Candidate
         with open(tmp, "rb+") as f:
             os.fsync(f.fileno())
         os.replace(tmp, path)
+        _fsync_dir(out_dir)
         rec = ChunkRecord(index=c, lo=lo, hi=hi, file=name, input_sha256=in_sha, file_sha256=_sha256_file(path),
                           edges=int(res.edges), transitions=int(res.transitions),
                           min_dist=int(dist.min()) if dist.size else 0, max_dist=int(dist.max()) if dist.size else 0)
@@ -182,4 +197,5 @@ def merge_edge_files(out_dir: str, out_path: str, ranks: int = 1) -> int:
                     w.write(blk)
             total += rec.hi - rec.lo
     os.replace(tmp, out_path)
+    _fsync_dir(os.path.dirname(os.path.abspath(out_path)))
     return total
