@@ -173,18 +173,24 @@ def walk_to_edge_files(states, out_dir: str, spec: CipherSpec, params: Candidate
 def merge_edge_files(out_dir: str, out_path: str, ranks: int = 1) -> int:
     """Concatenate every rank's chunk files in start order into one edge file; returns the
     record count.  Raises if a chunk is missing or its bytes changed."""
-    recs = []
+    recs, n = [], None
     for r in range(ranks):
         cfg, done = read_manifest(out_dir, r)
         if cfg is None:
             raise ValueError(f"no manifest for rank {r} in {out_dir}")
+        if n is not None and cfg["n"] != n:
+            raise ValueError("the ranks' manifests describe different start sets")
+        n = cfg["n"]
         recs.extend(done.values())
     recs.sort(key=lambda x: x.lo)
     pos = 0
     for rec in recs:
         if rec.lo != pos:
-            raise ValueError(f"chunk starting at {pos} is missing")
+            raise ValueError(f"chunk starting at {pos} is missing" if rec.lo > pos
+                             else f"chunk starting at {rec.lo} is listed twice")
         pos = rec.hi
+    if pos != n:
+        raise ValueError(f"chunks after record {pos} of {n} are missing")
     total = 0
     tmp = out_path + ".tmp"
     with open(tmp, "wb") as w:

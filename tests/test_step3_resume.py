@@ -85,6 +85,8 @@ def test_rank_shares_cover_the_set(tmp_path, fake):
     assert [r.lo for s in shares for r in s] == list(range(0, 1000, 100))
     assert step3.merge_edge_files(out, str(tmp_path / "all.bin"), ranks=3) == 1000
     assert (tmp_path / "all.bin").read_bytes() == _expected(states, 3)
+    with pytest.raises(ValueError):  # rank 2's chunks (the tail) not merged in
+        step3.merge_edge_files(out, str(tmp_path / "part.bin"), ranks=2)
 
 
 def test_torn_manifest_line_is_ignored(tmp_path, fake):
