@@ -137,6 +137,24 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+#ifndef LC_SORT_GATHER
+#define LC_SORT_GATHER 3  // payload gather: 0 two 16-B .nc loads, 1 two 16-B .cg, 2 one 32-B .nc, 3 one 32-B .cg
+#endif
+// one 32-byte payload record (a random sector of the record-major payload)
+__device__ __forceinline__ void gather32(const ulonglong2* __restrict__ aos, uint64_t r, ulonglong2& a, ulonglong2& b) {
+#if LC_SORT_GATHER == 0
+  a = aos[2 * r];
+  b = aos[2 * r + 1];
+#elif LC_SORT_GATHER == 1
+  a = __ldcg(aos + 2 * r);
+  b = __ldcg(aos + 2 * r + 1);
+#elif LC_SORT_GATHER == 2
+  asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a.x), "=l"(a.y), "=l"(b.x), "=l"(b.y) : "l"(aos + 2 * r));
+#else
+  asm("ld.global.cg.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a.x), "=l"(a.y), "=l"(b.x), "=l"(b.y) : "l"(aos + 2 * r));
+#endif
+}
+
 // Also packs the payload columns record-major (32 B per record: destination, distance,
 // subtree size, subtree depth; missing columns as 0), so the last pass fetches one
 // aligned 32-byte sector per record instead of one scattered sector per column.
@@ -238,6 +256,7 @@ constexpr int kWhistStride = kBins + 1;  // one spare counter per warp for lanes
 constexpr size_t kSmemKeys = kTileKeys * 8, kSmemRows = kTileKeys * 4;
 constexpr size_t kPassSmem = kSmemKeys + 2 * kSmemRows + (kSortWarps * kWhistStride + 8) * 4 + kBins * 8 + kBins * 4;
 
+template <bool kPersistent>
 __global__ void __launch_bounds__(kSortThreads, LC_SORT_MINBLOCKS) sort_pass_kernel(PassBufs bufs, Cols cols, uint64_t n, int byte,
                                                                     SortCtl* ctl, uint64_t* status,
                                                                     const ulonglong2* __restrict__ aos,
@@ -255,154 +274,160 @@ __global__ void __launch_bounds__(kSortThreads, LC_SORT_MINBLOCKS) sort_pass_ker
   __shared__ uint32_t wsum[kBins / 32];
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  if (tid == 0) tile_s = atomicAdd(&ctl->tickets[byte], 1u);
-  for (int i = tid; i < kSortWarps * kWhistStride; i += kSortThreads) whist[i] = 0;
-  __syncthreads();
-  const uint64_t tile = tile_s;
-  const uint64_t t0 = tile * kTileKeys;
-  const uint32_t tn = static_cast<uint32_t>(n - t0 < static_cast<uint64_t>(kTileKeys) ? n - t0 : kTileKeys);
-  const uint32_t ib = ctl->in_buf[byte];
-  const bool first = ib == 2u, last = ctl->last[byte] != 0u;
-  const uint64_t* __restrict__ kin = first ? cols.in[0] : bufs.keys[ib];
-  const int shift = static_cast<int>(ctl->shift[byte]);
-  const uint32_t dmask = ctl->dmask[byte];
+  const uint64_t ntiles = (n + kTileKeys - 1) / kTileKeys;
+  // persistent: a grid of resident blocks each taking tiles until none is left (the
+  // launches that usually return at once: the LSD passes behind the MSD route)
+  for (;;) {
+    if (tid == 0) tile_s = atomicAdd(&ctl->tickets[byte], 1u);
+    for (int i = tid; i < kSortWarps * kWhistStride; i += kSortThreads) whist[i] = 0;
+    __syncthreads();
+    const uint64_t tile = tile_s;
+    if (tile >= ntiles) return;  // block-uniform
+    const uint64_t t0 = tile * kTileKeys;
+    const uint32_t tn = static_cast<uint32_t>(n - t0 < static_cast<uint64_t>(kTileKeys) ? n - t0 : kTileKeys);
+    const uint32_t ib = ctl->in_buf[byte];
+    const bool first = ib == 2u, last = ctl->last[byte] != 0u;
+    const uint64_t* __restrict__ kin = first ? cols.in[0] : bufs.keys[ib];
+    const int shift = static_cast<int>(ctl->shift[byte]);
+    const uint32_t dmask = ctl->dmask[byte];
 
-  // ---- the row payload to shared memory in input order (async), keys to registers
-  if (!first) {
-    const uint32_t* __restrict__ rin = bufs.rows[ib] + t0;
-    if (tn == static_cast<uint32_t>(kTileKeys)) {
-      for (int c = tid; c < kTileKeys / 4; c += kSortThreads) cp_async16(irows + 4 * c, rin + 4 * c);
+    // ---- the row payload to shared memory in input order (async), keys to registers
+    if (!first) {
+      const uint32_t* __restrict__ rin = bufs.rows[ib] + t0;
+      if (tn == static_cast<uint32_t>(kTileKeys)) {
+        for (int c = tid; c < kTileKeys / 4; c += kSortThreads) cp_async16(irows + 4 * c, rin + 4 * c);
+      } else {
+        for (uint32_t j = tid; j < tn; j += kSortThreads) irows[j] = rin[j];
+      }
+    }
+    uint64_t key[kItems];
+    uint32_t rank[kItems];
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const uint32_t j = static_cast<uint32_t>(w * (32 * kItems) + k * 32 + lane);
+      key[k] = j < tn ? kin[t0 + j] : ~0ull;
+    }
+    // ---- rank within the warp (warp-striped: item k of lane l is tile key w*32*kItems + k*32 + l)
+    uint32_t* wh = whist + w * kWhistStride;
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const uint32_t j = static_cast<uint32_t>(w * (32 * kItems) + k * 32 + lane);
+      const uint32_t d = j < tn ? static_cast<uint32_t>(key[k] >> shift) & dmask : static_cast<uint32_t>(kBins);
+      const uint32_t peers = peers_of(d);
+      const uint32_t before = wh[d];
+      __syncwarp();
+      rank[k] = before + __popc(peers & lt);
+      if ((peers & lt) == 0u) wh[d] = before + __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+
+    // ---- digit d (thread d < 256): warp prefixes, tile count, publish, tile-local offsets
+    const int d = tid;
+    const bool owns_digit = tid < kBins;  // whole warps
+    uint32_t cnt = 0, incl = 0;
+    const uint64_t epoch = static_cast<uint64_t>(ctl->epoch_base + byte + 1) << 40;
+    volatile uint64_t* st = status;
+    if (owns_digit) {
+#pragma unroll
+      for (int v = 0; v < kSortWarps; ++v) {
+        const uint32_t c = whist[v * kWhistStride + d];
+        whist[v * kWhistStride + d] = cnt;
+        cnt += c;
+      }
+      if (tile == 0) st[d] = kFlagPrefix | epoch | cnt;
+      else st[tile * kBins + d] = kFlagAgg | epoch | cnt;
+      incl = cnt;  // tile-local exclusive scan over the digits
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(kFullMask, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (lane == 31) wsum[w] = incl;
+    }
+    __syncthreads();
+    if (owns_digit) {
+      uint32_t wpre = 0;
+#pragma unroll
+      for (int v = 0; v < kBins / 32; ++v) wpre += v < w ? wsum[v] : 0u;
+      loff[d] = wpre + incl - cnt;
+      uint64_t excl = 0;  // decoupled look-back: this digit's offset among earlier tiles
+      if (tile > 0) {
+        for (int64_t p = static_cast<int64_t>(tile) - 1; p >= 0; --p) {
+          uint64_t sv;
+          do {
+            sv = st[p * kBins + d];
+          } while ((sv & (0xffull << 40)) != epoch || (sv & (3ull << 48)) == 0);
+          excl += sv & kValueMask;
+          if (sv & kFlagPrefix) break;
+        }
+        st[tile * kBins + d] = kFlagPrefix | epoch | (excl + cnt);
+      }
+      gbase[d] = ctl->hist[byte][d] + excl;
+    }
+    if (!first) cp_async_wait_all();
+    __syncthreads();
+
+    // ---- stage the tile in digit order
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const uint32_t j = static_cast<uint32_t>(w * (32 * kItems) + k * 32 + lane);
+      if (j < tn) {
+        const uint32_t dg = static_cast<uint32_t>(key[k] >> shift) & dmask;
+        const uint32_t pos = loff[dg] + whist[w * kWhistStride + dg] + rank[k];
+        LC_CHECK(pos < static_cast<uint32_t>(kTileKeys));
+        skeys[pos] = key[k];
+        srows[pos] = first ? static_cast<uint32_t>(t0 + j) : irows[j];
+      }
+    }
+    __syncthreads();
+
+    // ---- write each digit's run contiguously; the last pass gathers the payload columns
+    if (!last) {
+      const uint32_t ob = first ? 1u - (ctl->passes & 1u) : ib ^ 1u;  // (passes - 1) & 1 for pass 0
+      uint64_t* __restrict__ kout = bufs.keys[ob];
+      uint32_t* __restrict__ rout = bufs.rows[ob];
+      for (uint32_t j = tid; j < tn; j += kSortThreads) {
+        const uint64_t k = skeys[j];
+        const uint32_t dg = static_cast<uint32_t>(k >> shift) & dmask;
+        const uint64_t o = gbase[dg] + (j - loff[dg]);
+        LC_CHECK(o < n && j >= loff[dg]);
+        kout[o] = k;
+        rout[o] = srows[j];
+      }
     } else {
-      for (uint32_t j = tid; j < tn; j += kSortThreads) irows[j] = rin[j];
-    }
-  }
-  uint64_t key[kItems];
-  uint32_t rank[kItems];
+      uint64_t* __restrict__ kout = cols.out[0];
+      constexpr int U = 4;  // records per thread per round: U payload sectors in flight
+      for (uint32_t j0 = tid; j0 < tn; j0 += kSortThreads * U) {
+        uint64_t o[U];
+        ulonglong2 a[U], b[U];
 #pragma unroll
-  for (int k = 0; k < kItems; ++k) {
-    const uint32_t j = static_cast<uint32_t>(w * (32 * kItems) + k * 32 + lane);
-    key[k] = j < tn ? kin[t0 + j] : ~0ull;
-  }
-  // ---- rank within the warp (warp-striped: item k of lane l is tile key w*32*kItems + k*32 + l)
-  uint32_t* wh = whist + w * kWhistStride;
-  const uint32_t lt = lanemask_lt();
-#pragma unroll
-  for (int k = 0; k < kItems; ++k) {
-    const uint32_t j = static_cast<uint32_t>(w * (32 * kItems) + k * 32 + lane);
-    const uint32_t d = j < tn ? static_cast<uint32_t>(key[k] >> shift) & dmask : static_cast<uint32_t>(kBins);
-    const uint32_t peers = peers_of(d);
-    const uint32_t before = wh[d];
-    __syncwarp();
-    rank[k] = before + __popc(peers & lt);
-    if ((peers & lt) == 0u) wh[d] = before + __popc(peers);
-    __syncwarp();
-  }
-  __syncthreads();
-
-  // ---- digit d (thread d < 256): warp prefixes, tile count, publish, tile-local offsets
-  const int d = tid;
-  const bool owns_digit = tid < kBins;  // whole warps
-  uint32_t cnt = 0, incl = 0;
-  const uint64_t epoch = static_cast<uint64_t>(ctl->epoch_base + byte + 1) << 40;
-  volatile uint64_t* st = status;
-  if (owns_digit) {
-#pragma unroll
-    for (int v = 0; v < kSortWarps; ++v) {
-      const uint32_t c = whist[v * kWhistStride + d];
-      whist[v * kWhistStride + d] = cnt;
-      cnt += c;
-    }
-    if (tile == 0) st[d] = kFlagPrefix | epoch | cnt;
-    else st[tile * kBins + d] = kFlagAgg | epoch | cnt;
-    incl = cnt;  // tile-local exclusive scan over the digits
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(kFullMask, incl, o);
-      if (lane >= o) incl += v;
-    }
-    if (lane == 31) wsum[w] = incl;
-  }
-  __syncthreads();
-  if (owns_digit) {
-    uint32_t wpre = 0;
-#pragma unroll
-    for (int v = 0; v < kBins / 32; ++v) wpre += v < w ? wsum[v] : 0u;
-    loff[d] = wpre + incl - cnt;
-    uint64_t excl = 0;  // decoupled look-back: this digit's offset among earlier tiles
-    if (tile > 0) {
-      for (int64_t p = static_cast<int64_t>(tile) - 1; p >= 0; --p) {
-        uint64_t sv;
-        do {
-          sv = st[p * kBins + d];
-        } while ((sv & (0xffull << 40)) != epoch || (sv & (3ull << 48)) == 0);
-        excl += sv & kValueMask;
-        if (sv & kFlagPrefix) break;
-      }
-      st[tile * kBins + d] = kFlagPrefix | epoch | (excl + cnt);
-    }
-    gbase[d] = ctl->hist[byte][d] + excl;
-  }
-  if (!first) cp_async_wait_all();
-  __syncthreads();
-
-  // ---- stage the tile in digit order
-#pragma unroll
-  for (int k = 0; k < kItems; ++k) {
-    const uint32_t j = static_cast<uint32_t>(w * (32 * kItems) + k * 32 + lane);
-    if (j < tn) {
-      const uint32_t dg = static_cast<uint32_t>(key[k] >> shift) & dmask;
-      const uint32_t pos = loff[dg] + whist[w * kWhistStride + dg] + rank[k];
-      LC_CHECK(pos < static_cast<uint32_t>(kTileKeys));
-      skeys[pos] = key[k];
-      srows[pos] = first ? static_cast<uint32_t>(t0 + j) : irows[j];
-    }
-  }
-  __syncthreads();
-
-  // ---- write each digit's run contiguously; the last pass gathers the payload columns
-  if (!last) {
-    const uint32_t ob = first ? 1u - (ctl->passes & 1u) : ib ^ 1u;  // (passes - 1) & 1 for pass 0
-    uint64_t* __restrict__ kout = bufs.keys[ob];
-    uint32_t* __restrict__ rout = bufs.rows[ob];
-    for (uint32_t j = tid; j < tn; j += kSortThreads) {
-      const uint64_t k = skeys[j];
-      const uint32_t dg = static_cast<uint32_t>(k >> shift) & dmask;
-      const uint64_t o = gbase[dg] + (j - loff[dg]);
-      LC_CHECK(o < n && j >= loff[dg]);
-      kout[o] = k;
-      rout[o] = srows[j];
-    }
-  } else {
-    uint64_t* __restrict__ kout = cols.out[0];
-    constexpr int U = 4;  // records per thread per round: U payload sectors in flight
-    for (uint32_t j0 = tid; j0 < tn; j0 += kSortThreads * U) {
-      uint64_t o[U];
-      ulonglong2 a[U], b[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t j = j0 + u * kSortThreads;
-        if (j < tn) {
-          const uint64_t k = skeys[j];
-          const uint32_t dg = static_cast<uint32_t>(k >> shift) & dmask;
-          o[u] = gbase[dg] + (j - loff[dg]);
-          LC_CHECK(o[u] < n && j >= loff[dg]);
-          kout[o[u]] = k;
-          const uint64_t r = srows[j];
-          a[u] = aos[2 * r];
-          b[u] = aos[2 * r + 1];
+        for (int u = 0; u < U; ++u) {
+          const uint32_t j = j0 + u * kSortThreads;
+          if (j < tn) {
+            const uint64_t k = skeys[j];
+            const uint32_t dg = static_cast<uint32_t>(k >> shift) & dmask;
+            o[u] = gbase[dg] + (j - loff[dg]);
+            LC_CHECK(o[u] < n && j >= loff[dg]);
+            kout[o[u]] = k;
+            gather32(aos, srows[j], a[u], b[u]);
+          }
         }
-      }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t j = j0 + u * kSortThreads;
-        if (j < tn) {
-          if (cols.out[1]) cols.out[1][o[u]] = a[u].x;
-          if (cols.out[2]) cols.out[2][o[u]] = a[u].y;
-          if (cols.out[3]) cols.out[3][o[u]] = b[u].x;
-          if (cols.out[4]) cols.out[4][o[u]] = b[u].y;
+        for (int u = 0; u < U; ++u) {
+          const uint32_t j = j0 + u * kSortThreads;
+          if (j < tn) {
+            if (cols.out[1]) cols.out[1][o[u]] = a[u].x;
+            if (cols.out[2]) cols.out[2][o[u]] = a[u].y;
+            if (cols.out[3]) cols.out[3][o[u]] = b[u].x;
+            if (cols.out[4]) cols.out[4][o[u]] = b[u].y;
+          }
         }
       }
     }
+    if (!kPersistent) return;
+    __syncthreads();  // the shared tile buffers and tile_s are reused
   }
 }
 
@@ -622,8 +647,7 @@ __global__ void __launch_bounds__(kLocalThreads, LC_SORT_LOCAL_MINBLOCKS) msd_lo
     for (int u = 0; u < U; ++u) {
       const uint32_t j = wbase + (k0 + u) * 32 + lane;
       if (j < size) {
-        a[u] = aos[2 * static_cast<uint64_t>(row[k0 + u])];
-        b[u] = aos[2 * static_cast<uint64_t>(row[k0 + u]) + 1];
+        gather32(aos, row[k0 + u], a[u], b[u]);
       }
     }
 #pragma unroll
@@ -723,6 +747,9 @@ cudaError_t radix_sort_records(uint64_t n, const uint64_t* const* cols_in, uint6
   p += align256(groups * 4);
   uint32_t* gend = reinterpret_cast<uint32_t*>(p);
   cudaError_t e;
+  if (const char* g = getenv("LFSR_SORT_L2FETCH")) {  // A/B: L2 fetch granularity hint
+    if ((e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(atoi(g)))) != cudaSuccess) return e;
+  }
   if ((e = cudaMemsetAsync(ctl, 0, sizeof(SortCtl), st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(mctl, 0, sizeof(SortCtl), st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(msd, 0, sizeof(MsdCtl), st)) != cudaSuccess) return e;
@@ -741,7 +768,9 @@ cudaError_t radix_sort_records(uint64_t n, const uint64_t* const* cols_in, uint6
   sort_init_kernel<<<1, 32, 0, st>>>(ctl, mctl);
   sort_hist_kernel<<<static_cast<unsigned>(hb), kSortThreads, 0, st>>>(cols_in[0], n, ctl, cols, aos, msd);
   sort_plan_kernel<<<1, kBins, 0, st>>>(n, ctl);
-  if ((e = cudaFuncSetAttribute(sort_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if ((e = cudaFuncSetAttribute(sort_pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kPassSmem))) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(sort_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(kPassSmem))) != cudaSuccess)
     return e;
   *launches += 3;
@@ -749,9 +778,10 @@ cudaError_t radix_sort_records(uint64_t n, const uint64_t* const* cols_in, uint6
     msd_plan_kernel<<<1, 1, 0, st>>>(n, W, ctl, mctl, msd);
     msd_hist_kernel<<<static_cast<unsigned>(hb), kSortThreads, 0, st>>>(cols_in[0], n, mctl, msd);
     sort_plan_kernel<<<1, kBins, 0, st>>>(n, mctl);
-    for (int sidx = 0; sidx < 3; ++sidx)
-      sort_pass_kernel<<<static_cast<unsigned>(tiles), kSortThreads, kPassSmem, st>>>(bufs, cols, n, sidx, mctl, status,
-                                                                                      aos, nullptr);
+    const int nd = static_cast<int>((W + 7) / 8);  // the window's digits (msd_plan_kernel)
+    for (int sidx = 0; sidx < nd; ++sidx)
+      sort_pass_kernel<false><<<static_cast<unsigned>(tiles), kSortThreads, kPassSmem, st>>>(bufs, cols, n, sidx, mctl,
+                                                                                             status, aos, nullptr);
     const uint64_t gb = std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(sms) * 16);
     msd_bounds_kernel<<<static_cast<unsigned>(gb), 256, 0, st>>>(cols_out[0], n, W, msd, gstart, gend);
     if ((e = cudaFuncSetAttribute(msd_local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -759,11 +789,20 @@ cudaError_t radix_sort_records(uint64_t n, const uint64_t* const* cols_in, uint6
       return e;
     msd_local_kernel<<<static_cast<unsigned>(groups), kLocalThreads, kLocalSmem, st>>>(bufs, cols, msd, gstart, gend,
                                                                                       aos);
-    *launches += 8;
+    *launches += 5 + nd;
   }
-  for (int b = 0; b < kBytes; ++b)  // trivial bytes return at once (decided on the device)
-    sort_pass_kernel<<<static_cast<unsigned>(tiles), kSortThreads, kPassSmem, st>>>(bufs, cols, n, b, ctl, status, aos,
-                                                                                    msd);
+  // trivial bytes return at once (decided on the device); behind the MSD route the passes
+  // run only on its fallback, so they are launched persistent: a few resident blocks that
+  // return at once rather than a block per tile
+  const uint64_t pgrid = std::min<uint64_t>(tiles, static_cast<uint64_t>(sms) * LC_SORT_MINBLOCKS);
+  for (int b = 0; b < kBytes; ++b) {
+    if (W)
+      sort_pass_kernel<true><<<static_cast<unsigned>(pgrid), kSortThreads, kPassSmem, st>>>(bufs, cols, n, b, ctl,
+                                                                                            status, aos, msd);
+    else
+      sort_pass_kernel<false><<<static_cast<unsigned>(tiles), kSortThreads, kPassSmem, st>>>(bufs, cols, n, b, ctl,
+                                                                                             status, aos, msd);
+  }
   const uint64_t gb = std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(sms) * 8);
   sort_copy_kernel<<<static_cast<unsigned>(gb), 256, 0, st>>>(n, ctl, cols, msd);
   *launches += kBytes + 1;
