@@ -496,7 +496,19 @@ __global__ void __launch_bounds__(kSortThreads) msd_hist_kernel(const uint64_t* 
   __syncthreads();
   const unsigned int nd = m->nslots;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kSortThreads;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kSortThreads + threadIdx.x; i < n; i += stride) {
+  const uint64_t t = static_cast<uint64_t>(blockIdx.x) * kSortThreads + threadIdx.x;
+  const uint64_t n4 = (reinterpret_cast<uintptr_t>(keys) & 15u) == 0 ? n / 4 : 0;  // four keys per thread and round
+  const ulonglong2* __restrict__ k2 = reinterpret_cast<const ulonglong2*>(keys);
+  for (uint64_t q = t; q < n4; q += stride) {
+    const ulonglong2 a = k2[2 * q], c = k2[2 * q + 1];
+    const uint64_t k[4] = {a.x, a.y, c.x, c.y};
+    for (unsigned int b = 0; b < nd; ++b) {
+      const unsigned int shb = m->shift[b], mb = m->dmask[b];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) atomicAdd(&h[b][static_cast<uint32_t>(k[j] >> shb) & mb], 1u);
+    }
+  }
+  for (uint64_t i = 4 * n4 + t; i < n; i += stride) {
     const uint64_t k = keys[i];
     for (unsigned int b = 0; b < nd; ++b) atomicAdd(&h[b][static_cast<uint32_t>(k >> m->shift[b]) & m->dmask[b]], 1u);
   }
@@ -507,14 +519,30 @@ __global__ void __launch_bounds__(kSortThreads) msd_hist_kernel(const uint64_t* 
   }
 }
 
-// group g = records whose window equals g: [start[g], end[g]) of the MSD-sorted keys
+// group g = records whose window equals g: [start[g], end[g]) of the MSD-sorted keys;
+// four keys per thread and round (two 16-byte loads: enough bytes in flight for HBM),
+// the neighbours across the quad from L1 / L2
 __global__ void msd_bounds_kernel(const uint64_t* __restrict__ keys, uint64_t n, uint32_t W, const MsdCtl* msd,
                                   uint32_t* __restrict__ gstart, uint32_t* __restrict__ gend) {
   if (!msd->use_msd) return;
   const uint32_t sh = msd->win_shift;
   const uint64_t wm = (1ull << W) - 1ull;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t n4 = (reinterpret_cast<uintptr_t>(keys) & 15u) == 0 ? n / 4 : 0;
+  const ulonglong2* __restrict__ k2 = reinterpret_cast<const ulonglong2*>(keys);
+  for (uint64_t q = t; q < n4; q += stride) {
+    const ulonglong2 a = k2[2 * q], b = k2[2 * q + 1];
+    const uint64_t i = 4 * q;
+    const uint64_t g[6] = {i == 0 ? ~0ull : (keys[i - 1] >> sh) & wm, (a.x >> sh) & wm, (a.y >> sh) & wm,
+                           (b.x >> sh) & wm, (b.y >> sh) & wm, i + 4 >= n ? ~0ull : (keys[i + 4] >> sh) & wm};
+#pragma unroll
+    for (int j = 1; j <= 4; ++j) {
+      if (g[j - 1] != g[j]) gstart[g[j]] = static_cast<uint32_t>(i + j - 1);
+      if (g[j + 1] != g[j]) gend[g[j]] = static_cast<uint32_t>(i + j);
+    }
+  }
+  for (uint64_t i = 4 * n4 + t; i < n; i += stride) {
     const uint64_t g = (keys[i] >> sh) & wm;
     if (i == 0 || ((keys[i - 1] >> sh) & wm) != g) gstart[g] = static_cast<uint32_t>(i);
     if (i + 1 == n || ((keys[i + 1] >> sh) & wm) != g) gend[g] = static_cast<uint32_t>(i + 1);
