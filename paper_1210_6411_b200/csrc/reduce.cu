@@ -7,7 +7,9 @@
 // Destinations are resolved once to record indices by binary search; every pass is then
 // a handful of streaming kernels: mark in-degree, fold each leaf's (size+1, depth+1) into
 // its destination with atomics (leaves are never targets within a pass, so the reads are
-// stable), and a stable compaction that also remaps destination indices.  The result is
+// stable), and a stable compaction that also remaps destination indices; once the
+// frontier fits in shared memory one block runs the remaining passes (cut_tail_kernel),
+// a block barrier per pass instead of two launches.  The result is
 // the reference's fixpoint and per-pass statistics exactly, without external sorts.
 // Cycles: pointer jumping labels every record with the smallest index on its cycle (the
 // smallest source, since sources ascend), then one atomic fold per record.
@@ -224,6 +226,96 @@ __global__ void cut_pass_end_kernel(CutCtl* ctl, int w, uint64_t* __restrict__ p
   ctl->sum += leaves;
   ctl->cnt[w] = 0;
   if (leaves == 0 && ctl->done_at == 0) ctl->done_at = p;
+}
+
+// The tail of a cut: a frontier never grows (each new leaf is the destination of at least
+// one leaf of the pass before), so once it fits in shared memory one block runs the
+// passes itself -- the fold, a block barrier, the pass bookkeeping of cut_pass_end_kernel
+// -- instead of two launches per pass.  Entered at parity 0 (after the graph's two wide
+// passes); runs passes in pairs so it leaves at parity 0, until the fixpoint or `budget`
+// passes.  Sizes and depths are read at L2 (ld.cg): earlier passes of this kernel changed
+// them by atomics, which the L1 would not see.  A frontier entry carries its record's
+// destination, loaded while the pass that made it a leaf waits on its in-degree atomic,
+// so a pass's dependent chain is one L2 atomic round trip rather than a load and then one.
+constexpr int kTailThreads = 1024;
+constexpr uint32_t kTailMax = 6144;  // frontier entries per buffer (2 x 96 KB of shared memory)
+constexpr size_t kTailSmem = 2 * kTailMax * sizeof(ulonglong2);
+
+__global__ void __launch_bounds__(kTailThreads) cut_tail_kernel(CutCtl* ctl, uint64_t* __restrict__ f0,
+                                                                const uint64_t* __restrict__ idx,
+                                                                unsigned long long* size, unsigned long long* depth,
+                                                                unsigned int* indeg, uint8_t* __restrict__ alive,
+                                                                unsigned int* err, uint64_t* __restrict__ pstats,
+                                                                uint64_t max_stats, uint32_t budget) {
+  const unsigned long long m0 = ctl->cnt[0];
+  if (m0 > kTailMax || ctl->done_at) return;  // still wide, or past the fixpoint
+  extern __shared__ ulonglong2 tf[];          // [2][kTailMax]: (record, its destination)
+  // frontier sizes rotate over three counters, so one barrier per pass suffices: pass q
+  // reads tcnt[q % 3], appends to tcnt[(q + 1) % 3] and clears tcnt[(q + 2) % 3] (read
+  // by pass q - 1, before the last barrier; appended to by pass q + 1, after the next)
+  __shared__ unsigned int tcnt[3];
+  const int tid = threadIdx.x;
+  for (uint32_t k = tid; k < m0; k += kTailThreads) {
+    const uint64_t i = f0[k];
+    tf[k] = make_ulonglong2(i, idx[i]);
+  }
+  unsigned long long t_alive = 0, t_sum = 0, t_pass = 0, t_done = 0;  // thread 0's bookkeeping
+  if (tid == 0) {
+    tcnt[0] = static_cast<unsigned int>(m0);
+    tcnt[1] = tcnt[2] = 0;
+    t_alive = ctl->alive;
+    t_sum = ctl->sum;
+    t_pass = ctl->pass;
+  }
+  __syncthreads();
+  bool done = false;
+  uint32_t q = 0;
+  while (q < budget) {
+    const int w = static_cast<int>(q & 1u), c = static_cast<int>(q % 3u);
+    const uint32_t m = tcnt[c];
+    const ulonglong2* fc = tf + w * kTailMax;
+    ulonglong2* fn = tf + (w ^ 1) * kTailMax;
+    unsigned int* cnext = &tcnt[(c + 1) % 3];
+    for (uint32_t k = tid; k < m; k += kTailThreads) {
+      const uint64_t i = fc[k].x, j = fc[k].y;
+      alive[i] = 0;
+      if (j == kNone) {
+        atomicExch(err, 2u);
+      } else {
+        const uint64_t jj = idx[j];  // in flight with the in-degree atomic
+        const bool leaf = atomicSub(&indeg[j], 1u) == 1u;
+        atomicAdd(&size[j], __ldcg(&size[i]) + 1ull);
+        atomicMax(&depth[j], __ldcg(&depth[i]) + 1ull);
+        if (leaf) fn[atomicAdd(cnext, 1u)] = make_ulonglong2(j, jj);
+      }
+    }
+    if (tid == 0) {  // cut_pass_end_kernel's bookkeeping
+      const unsigned long long p = ++t_pass;
+      if (p - 1 < max_stats) {
+        pstats[3 * (p - 1) + 0] = m;
+        pstats[3 * (p - 1) + 1] = t_alive - m;
+        pstats[3 * (p - 1) + 2] = t_sum + m;
+      }
+      t_alive -= m;
+      t_sum += m;
+      if (m == 0 && t_done == 0) t_done = p;
+      tcnt[(c + 2) % 3] = 0;
+    }
+    done |= m == 0;  // block-uniform
+    __syncthreads();
+    ++q;
+    if (done && !(q & 1u)) break;  // leave at parity 0
+  }
+  const uint32_t mq = tcnt[q % 3];
+  for (uint32_t k = tid; k < mq; k += kTailThreads) f0[k] = tf[k].x;
+  if (tid == 0) {
+    ctl->cnt[0] = mq;
+    ctl->cnt[1] = 0;
+    ctl->alive = t_alive;
+    ctl->sum = t_sum;
+    ctl->pass = t_pass;
+    ctl->done_at = t_done;
+  }
 }
 
 // ---- sharded leaf cutting (multi-GPU step 4).  Each rank holds one contiguous source
@@ -501,6 +593,7 @@ cudaError_t cut_leaves_device(uint64_t n, uint64_t* src, uint64_t* dst, uint64_t
     cut_pass_end_kernel<<<1, 1, 0, st>>>(ctl, w, pstats, max_stats);
   };
   constexpr int kLaunchesPerPass = 2;
+  constexpr uint32_t kTailBudget = 1024;  // tail passes per graph replay (even)
   CutCtl h{};
   uint64_t executed = 0;
   if (max_passes != 0) {
@@ -513,17 +606,21 @@ cudaError_t cut_leaves_device(uint64_t n, uint64_t* src, uint64_t* dst, uint64_t
   } else {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
+    if ((e = cudaFuncSetAttribute(cut_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kTailSmem))) != cudaSuccess)
+      return e;
     if ((e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) return e;
     pass(0);
     pass(1);
+    cut_tail_kernel<<<1, kTailThreads, kTailSmem, st>>>(ctl, f0, idx, usize, udepth, indeg, alive, err, pstats, max_stats,
+                                                        kTailBudget);
     if ((e = cudaStreamEndCapture(st, &graph)) != cudaSuccess) return e;
     if ((e = cudaGraphInstantiate(&exec, graph, 0)) != cudaSuccess) return e;
     for (int batch = 8;; batch = std::min(batch * 2, 512)) {  // graphs (x2 passes) per host check-in
       for (int k = 0; k < batch; ++k)
         if ((e = cudaGraphLaunch(exec, st)) != cudaSuccess) break;
       if (e != cudaSuccess) break;
-      executed += 2 * batch;
-      *launches += 2 * batch * kLaunchesPerPass;
+      *launches += batch * (2 * kLaunchesPerPass + 1);
       if ((e = cudaMemcpyAsync(&h, ctl, sizeof(h), cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
       if ((e = cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
       if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
@@ -537,7 +634,7 @@ cudaError_t cut_leaves_device(uint64_t n, uint64_t* src, uint64_t* dst, uint64_t
     *err_out = herr;
     return cudaSuccess;
   }
-  const uint64_t passes = h.done_at ? h.done_at : executed;
+  const uint64_t passes = h.done_at ? h.done_at : (max_passes != 0 ? executed : h.pass);
   *n_passes = static_cast<uint32_t>(passes);
   const uint64_t keep_stats = std::min<uint64_t>(passes, max_stats);
   if (keep_stats)

@@ -143,7 +143,7 @@ def cut_leaves_arrays(src, dst, dist, subtree_size, subtree_depth, *, max_passes
             break
         cap = int(npass.value)
     m = int(nout.value)
-    passes = [tuple(int(v) for v in stats[i]) for i in range(min(int(npass.value), cap))]
+    passes = [tuple(r) for r in stats[: min(int(npass.value), cap)].tolist()]
     return tuple(c[:m] for c in cols) + (passes,)
 
 
@@ -170,7 +170,7 @@ def cut_leaves_tensors(src, dst, dist, subtree_size, subtree_depth, *, max_passe
                                     N.u64p(stats), cap, C.byref(npass), C.byref(nout), stream)
     if rc != N.LC_OK:
         _raise(rc)
-    passes = [tuple(int(v) for v in stats[i]) for i in range(min(int(npass.value), cap))]
+    passes = [tuple(r) for r in stats[: min(int(npass.value), cap)].tolist()]
     return int(nout.value), passes
 
 
