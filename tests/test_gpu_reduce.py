@@ -129,3 +129,36 @@ def test_write_edge_tensors_byte_identical(gpu, tmp_path):
     assert (tmp_path / "c.bin").read_bytes() == (tmp_path / "d.bin").read_bytes()
     write_edge_tensors(tmp_path / "e.bin", *(x[:0] for x in t[:3]))
     assert (tmp_path / "e.bin").read_bytes() == b""
+
+
+@pytest.mark.parametrize("shape", ["path", "broom"])
+def test_long_tail_of_passes_matches_restatement(gpu, lc, shape):
+    """Thousands of passes with tiny frontiers: the single-block tail kernel (csrc/reduce.cu
+    cut_tail_kernel) runs them, across several graph replays (1024 tail passes each), and
+    must give the restatement's per-pass statistics exactly.  "path": one 3000-record chain
+    into a self-loop (one leaf per pass); "broom": a 2^16-node random forest (wide passes
+    first) whose roots hang off a 2500-record chain."""
+    from oracle import reduce_np
+
+    rng = np.random.default_rng(11)
+    if shape == "path":
+        n = 3000
+        dst_idx = np.minimum(np.arange(n) + 1, n - 1)
+    else:
+        chain, bush = 2500, 1 << 16
+        n = chain + bush
+        dst_idx = np.empty(n, dtype=np.int64)
+        dst_idx[:chain] = np.minimum(np.arange(chain) + 1, chain - 1)
+        dst_idx[chain:] = rng.integers(0, chain // 8, size=bush)  # trees rooted near the chain's start
+        inner = rng.random(bush) < 0.7
+        dst_idx[chain:][inner] = chain + rng.integers(0, bush, size=int(inner.sum()))
+    src = np.sort(rng.choice(np.uint64(1) << np.uint64(50), size=n, replace=False).astype(np.uint64))
+    dst = src[dst_idx]
+    dist = rng.integers(1, 1000, size=n, dtype=np.uint64)
+    z = np.zeros(n, dtype=np.uint64)
+    got = lc.cut_leaves_arrays(src, dst, dist, z, z)
+    want = reduce_np.cut_leaves(src, dst, dist, z, z)
+    assert got[5] == want[5]
+    assert len(got[5]) > 2000
+    for a, b in zip(got[:5], want[:5]):
+        assert (a == b).all()
