@@ -1087,6 +1087,7 @@ int lc_cut_leaves_device(lc_ctx* ctx, uint64_t n, uint64_t* src, uint64_t* dst, 
   LC_CUDA(lc::cut_leaves_device(n, src, dst, dist, subtree_size, subtree_depth, max_passes, pass_stats, max_stats,
                                 n_passes, n_out, &err, ctx->scratch.p, ctx->stream, &launches));
   g_launches += launches;
+  LC_CUDA(cudaStreamSynchronize(ctx->stream));  // the compaction's last copies are still queued
   return err ? reduce_error(err) : LC_OK;
 }
 
