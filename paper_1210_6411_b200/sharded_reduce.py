@@ -22,11 +22,23 @@ Pass statistics follow from the counts alone: inner_nodes = alive - leaves, and 
 survivors' subtree-size sum grows by exactly the leaves removed.  The survivors end up
 compacted in place on each rank (source order), so the concatenation over ranks is the
 reference's output file.
+
+The tail.  A frontier never grows, and random mappings spend thousands of passes on a
+few leaves each, where the two collectives per pass are the whole cost.  Once a pass
+removes at most ``TAIL_LEAVES`` records and at most ``TAIL_ALIVE`` are still alive,
+every rank compacts its alive records (``lc_cut_shard_finish``), the alive records of
+all ranks are all-gathered (they form a closed graph: a survivor's destination
+survives), and every rank runs the single-GPU cut to the fixpoint on that copy
+(``reduce.cut_leaves_tensors``, deterministic: atomic sums and maxima) and keeps the
+survivors in its own source range.  Its pass statistics continue the global ones (its
+alive count and size sum are the global ones).  One all-gather instead of two
+collectives per remaining pass.
 """
 
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -35,6 +47,8 @@ from . import _native as N
 __all__ = ["NativeShard", "cut_leaves_sharded", "shard_bounds"]
 
 _U64 = (1 << 64) - 1
+TAIL_LEAVES = 1 << 16
+TAIL_ALIVE = 1 << 23
 
 
 class NativeShard:
@@ -67,6 +81,7 @@ class NativeShard:
         self.size_sum = int(s[0])
         self._counts = np.zeros(self.n_ranks, dtype=np.uint64)
         self._info = np.zeros(2, dtype=np.uint64)
+        self.gathers_tail = True  # the driver may finish the cut on gathered records
 
     def emit(self, phase: int):
         """-> (messages [m, 3] grouped by owner, per-owner counts, records emitted, error word)."""
@@ -144,6 +159,21 @@ class _Exchange:
         self.dist.all_to_all_single(recv, src.contiguous(), [int(c) for c in recv_counts],
                                     [int(c) for c in send_counts], group=self.group)
         return recv.to(send.device) if staged else recv
+
+    def allgather_rows(self, rows, counts):
+        """Every rank's [counts[r], k] int64 rows, concatenated in rank order."""
+        if self.solo:
+            return rows
+        torch = self.torch
+        staged = rows.is_cuda and not self.nccl
+        src = rows.cpu() if staged else rows
+        width, top = src.shape[1], int(max(counts))
+        pad = torch.zeros((top, width), dtype=torch.int64, device=src.device)
+        pad[: src.shape[0]] = src
+        out = [torch.empty_like(pad) for _ in range(self.world)]
+        self.dist.all_gather(out, pad, group=self.group)
+        cat = torch.cat([o[: int(c)] for o, c in zip(out, counts)])
+        return cat.to(rows.device) if staged else cat
 
 
 def _u64(x) -> int:
@@ -230,8 +260,46 @@ def _drive(ex, shard, total: int, max_passes: int):
         s = (s + removed) & _U64
         if removed == 0 or (max_passes and p >= max_passes):
             break
+        if (not max_passes and getattr(shard, "gathers_tail", False) and removed <= TAIL_LEAVES
+                and 0 < alive <= TAIL_ALIVE and os.environ.get("LFSR_SHARD_TAIL", "1") != "0"):
+            return _gathered_tail(ex, shard, passes, alive)
     n_out, rc = shard.finish()
     flags = ex.allgather([rc])
     if flags.any():
         raise ValueError("a removed leaf's destination has no surviving record; input was not closed")
     return n_out, passes
+
+
+def _gathered_tail(ex, shard, passes, alive: int):
+    """Finish the cut on the all-gathered alive records (module docstring, "The tail")."""
+    import torch
+
+    from .reduce import cut_leaves_tensors
+
+    n_loc, rc = shard.finish()  # this rank's alive records, compacted to the front in source order
+    mat = ex.allgather([rc, n_loc])
+    if mat[:, 0].any():
+        raise ValueError("a removed leaf's destination has no surviving record; input was not closed")
+    counts = mat[:, 1]
+    if int(counts.sum()) != alive:
+        raise RuntimeError(f"sharded leaf cutting: {int(counts.sum())} alive records gathered, {alive} expected")
+    cols = shard.cols
+    rows = ex.allgather_rows(torch.stack([c[:n_loc] for c in cols], 1), counts)
+    g = [rows[:, k].contiguous() for k in range(5)]
+    try:
+        n_fix, tail = cut_leaves_tensors(*g)
+    except ValueError as e:  # every rank runs the same cut: all of them raise
+        raise ValueError(f"a removed leaf's destination has no surviving record; input was not closed ({e})") from e
+    passes.extend(tail)
+    # the gathered survivors stay in source order: this rank's are the run between its own
+    # first and last alive source (unsigned order: compared with the sign bit flipped)
+    if not n_loc or not n_fix:
+        return 0, passes
+    flip = torch.iinfo(torch.int64).min
+    surv = g[0][:n_fix] ^ flip
+    ends = torch.stack([cols[0][0], cols[0][n_loc - 1]]) ^ flip
+    a = int(torch.searchsorted(surv, ends[:1]).item())
+    b = int(torch.searchsorted(surv, ends[1:], right=True).item())
+    for k in range(5):
+        cols[k][: b - a] = g[k][a:b]
+    return b - a, passes
