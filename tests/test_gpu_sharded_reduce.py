@@ -84,11 +84,16 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out, backend="gloo"):
+def _two_rank_cases():
+    # the 2^18 mapping's first pass removes more than TAIL_LEAVES: the gathered tail starts later
+    return {"mini789": _mini789(), "random": _random_mapping(1 << 16, 5), "random_2p18": _random_mapping(1 << 18, 9)}
+
+
+def _worker(rank, world, port, out, backend="gloo", tail="1"):
     import torch
     import torch.distributed as dist
 
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), LFSR_SHARD_TAIL=tail)
     if backend == "nccl":
         torch.cuda.set_device(0)
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
@@ -98,7 +103,7 @@ def _worker(rank, world, port, out, backend="gloo"):
         from paper_1210_6411_b200.distributed import shard_range
         from paper_1210_6411_b200.sharded_reduce import cut_leaves_sharded
 
-        cases = {"mini789": _mini789(), "random": _random_mapping(1 << 16, 5)}
+        cases = _two_rank_cases()
         for name, cols in cases.items():
             lo, hi = shard_range(cols[0].size, rank, world)
             t = _tensors(cols, lo, hi)
@@ -108,15 +113,18 @@ def _worker(rank, world, port, out, backend="gloo"):
         dist.destroy_process_group()
 
 
-def test_sharded_two_ranks_on_one_gpu(gpu):
+@pytest.mark.parametrize("tail", ["1", "0"], ids=["gathered_tail", "per_pass_only"])
+def test_sharded_two_ranks_on_one_gpu(gpu, tail):
+    """Two gloo ranks (sharing this box's one GPU): with the gathered tail (the default:
+    after the first pass here) and with every pass exchanged."""
     import torch.multiprocessing as mp
     from oracle import reduce_np
 
     world = 2
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
-    for name, cols in {"mini789": _mini789(), "random": _random_mapping(1 << 16, 5)}.items():
+    mp.spawn(_worker, args=(world, _free_port(), out, "gloo", tail), nprocs=world, join=True)
+    for name, cols in _two_rank_cases().items():
         want = reduce_np.cut_leaves(*cols)
         rows = sum((out[(name, r)][0] for r in range(world)), [])
         assert rows == np.stack(want[:5], 1).tolist(), name
@@ -133,7 +141,7 @@ def test_sharded_one_rank_over_nccl(gpu):
     mgr = mp.Manager()
     out = mgr.dict()
     mp.spawn(_worker, args=(1, _free_port(), out, "nccl"), nprocs=1, join=True)
-    for name, cols in {"mini789": _mini789(), "random": _random_mapping(1 << 16, 5)}.items():
+    for name, cols in _two_rank_cases().items():
         want = reduce_np.cut_leaves(*cols)
         assert out[(name, 0)][0] == np.stack(want[:5], 1).tolist(), name
         assert out[(name, 0)][1] == [tuple(int(v) for v in p) for p in want[5]], name
