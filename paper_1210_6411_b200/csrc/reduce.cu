@@ -240,6 +240,10 @@ __global__ void cut_pass_end_kernel(CutCtl* ctl, int w, uint64_t* __restrict__ p
 constexpr int kTailThreads = 1024;
 constexpr uint32_t kTailMax = 6144;  // frontier entries per buffer (2 x 96 KB of shared memory)
 constexpr size_t kTailSmem = 2 * kTailMax * sizeof(ulonglong2);
+#ifndef LC_CUT_TAIL_WARP
+#define LC_CUT_TAIL_WARP 1
+#endif
+constexpr bool kTailWarpMode = LC_CUT_TAIL_WARP != 0;  // frontiers of <= 32: warp 0 alone
 
 __global__ void __launch_bounds__(kTailThreads) cut_tail_kernel(CutCtl* ctl, uint64_t* __restrict__ f0,
                                                                 const uint64_t* __restrict__ idx,
@@ -268,11 +272,27 @@ __global__ void __launch_bounds__(kTailThreads) cut_tail_kernel(CutCtl* ctl, uin
     t_pass = ctl->pass;
   }
   __syncthreads();
-  bool done = false;
+  // cut_pass_end_kernel's bookkeeping for a pass that removed m records (thread 0)
+  auto close_pass = [&](uint32_t m) {
+    const unsigned long long p = ++t_pass;
+    if (p - 1 < max_stats) {
+      pstats[3 * (p - 1) + 0] = m;
+      pstats[3 * (p - 1) + 1] = t_alive - m;
+      pstats[3 * (p - 1) + 2] = t_sum + m;
+    }
+    t_alive -= m;
+    t_sum += m;
+    if (m == 0 && t_done == 0) t_done = p;
+  };
+  bool done = false, narrow = false;
   uint32_t q = 0;
   while (q < budget) {
     const int w = static_cast<int>(q & 1u), c = static_cast<int>(q % 3u);
     const uint32_t m = tcnt[c];
+    if (m <= 32u && kTailWarpMode) {  // block-uniform; a frontier never grows again
+      narrow = true;
+      break;
+    }
     const ulonglong2* fc = tf + w * kTailMax;
     ulonglong2* fn = tf + (w ^ 1) * kTailMax;
     unsigned int* cnext = &tcnt[(c + 1) % 3];
@@ -289,16 +309,8 @@ __global__ void __launch_bounds__(kTailThreads) cut_tail_kernel(CutCtl* ctl, uin
         if (leaf) fn[atomicAdd(cnext, 1u)] = make_ulonglong2(j, jj);
       }
     }
-    if (tid == 0) {  // cut_pass_end_kernel's bookkeeping
-      const unsigned long long p = ++t_pass;
-      if (p - 1 < max_stats) {
-        pstats[3 * (p - 1) + 0] = m;
-        pstats[3 * (p - 1) + 1] = t_alive - m;
-        pstats[3 * (p - 1) + 2] = t_sum + m;
-      }
-      t_alive -= m;
-      t_sum += m;
-      if (m == 0 && t_done == 0) t_done = p;
+    if (tid == 0) {
+      close_pass(m);
       tcnt[(c + 2) % 3] = 0;
     }
     done |= m == 0;  // block-uniform
@@ -306,6 +318,54 @@ __global__ void __launch_bounds__(kTailThreads) cut_tail_kernel(CutCtl* ctl, uin
     ++q;
     if (done && !(q & 1u)) break;  // leave at parity 0
   }
+  // At most 32 leaves left per pass: warp 0 runs the remaining passes alone, one leaf per
+  // lane, the next frontier compacted into lanes by a ballot -- no shared-memory counters,
+  // no block barriers, only the warp's own synchronisation between passes.
+  __shared__ uint32_t q_end;
+  if (narrow && tid < 32) {
+    const uint32_t lane = tid;
+    uint32_t m = tcnt[q % 3u];
+    ulonglong2 e = lane < m ? tf[(q & 1u) * kTailMax + lane] : make_ulonglong2(0ull, kNone);
+    bool have = lane < m;
+    while (q < budget) {
+      bool push = false;
+      uint64_t j = 0, jj = 0;
+      if (have) {
+        const uint64_t i = e.x;
+        j = e.y;
+        alive[i] = 0;
+        if (j == kNone) {
+          atomicExch(err, 2u);
+        } else {
+          jj = idx[j];
+          push = atomicSub(&indeg[j], 1u) == 1u;
+          atomicAdd(&size[j], __ldcg(&size[i]) + 1ull);
+          atomicMax(&depth[j], __ldcg(&depth[i]) + 1ull);
+        }
+      }
+      const uint32_t pushed = __ballot_sync(0xffffffffu, push);
+      const uint32_t from = __fns(pushed, 0, lane + 1);  // the lane with the (lane+1)-th push
+      const uint32_t src_lane = from < 32u ? from : 0u;
+      e.x = __shfl_sync(0xffffffffu, j, src_lane);
+      e.y = __shfl_sync(0xffffffffu, jj, src_lane);
+      if (lane == 0) close_pass(m);
+      done |= m == 0;
+      m = __popc(pushed);
+      have = lane < m;
+      __syncwarp();  // this pass's folds before the next pass's reads
+      ++q;
+      if (done && !(q & 1u)) break;
+    }
+    if (have) tf[lane] = e;  // parity 0: buffer 0
+    if (lane == 0) {
+      tcnt[q % 3u] = m;
+      q_end = q;
+    }
+  } else if (!narrow && tid == 0) {
+    q_end = q;
+  }
+  __syncthreads();
+  q = q_end;
   const uint32_t mq = tcnt[q % 3];
   for (uint32_t k = tid; k < mq; k += kTailThreads) f0[k] = tf[k].x;
   if (tid == 0) {
