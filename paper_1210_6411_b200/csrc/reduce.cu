@@ -44,11 +44,40 @@ __global__ void check_sorted_kernel(const uint64_t* __restrict__ src, uint64_t n
   }
 }
 
+// Destination -> record index by binary search over the sorted sources, narrowed by a
+// directory of the B bits below the sources' common prefix: dir[b] = first record whose
+// bucket is >= b (the sources' highest varying bit is the highest bit of src[0] ^
+// src[n-1]), so a search covers one bucket (~n / 2^B records) instead of all n.
+__device__ __forceinline__ uint32_t dir_shift(const uint64_t* __restrict__ src, uint64_t n, int B) {
+  const uint64_t x = src[0] ^ src[n - 1];
+  const int top = x ? 64 - __clzll(static_cast<long long>(x)) : 0;  // varying bits [0, top)
+  return top > B ? static_cast<uint32_t>(top - B) : 0u;
+}
+
+__global__ void dir_build_kernel(const uint64_t* __restrict__ src, uint64_t n, int B, uint64_t* __restrict__ dir) {
+  const uint32_t sh = dir_shift(src, n, B);
+  const uint64_t bm = (1ull << B) - 1ull;
+  GRID_STRIDE(i, n) {
+    const uint64_t b = (src[i] >> sh) & bm;
+    const uint64_t from = i ? ((src[i - 1] >> sh) & bm) + 1ull : 0ull;
+    for (uint64_t t = from; t <= b; ++t) dir[t] = i;  // (an unsorted input is rejected anyway)
+    if (i + 1 == n)
+      for (uint64_t t = b + 1; t <= bm + 1; ++t) dir[t] = n;
+  }
+}
+
 __global__ void resolve_kernel(const uint64_t* __restrict__ src, uint64_t n, const uint64_t* __restrict__ dst,
-                               uint64_t* __restrict__ idx) {
+                               uint64_t* __restrict__ idx, int B, const uint64_t* __restrict__ dir) {
+  const uint32_t sh = B ? dir_shift(src, n, B) : 0u;
+  const uint64_t bm = (1ull << B) - 1ull;
   GRID_STRIDE(i, n) {
     const uint64_t v = dst[i];
     uint64_t lo = 0, hi = n;
+    if (B) {
+      const uint64_t b = (v >> sh) & bm;
+      lo = dir[b];
+      hi = dir[b + 1];
+    }
     while (lo < hi) {
       const uint64_t mid = (lo + hi) >> 1;
       if (src[mid] < v) lo = mid + 1;
@@ -56,6 +85,13 @@ __global__ void resolve_kernel(const uint64_t* __restrict__ src, uint64_t n, con
     }
     idx[i] = (lo < n && src[lo] == v) ? lo : kNone;
   }
+}
+
+// directory bits for n records: ~4-16 records per bucket, the directory within n entries
+inline int dir_bits(uint64_t n) {
+  if (n < (1ull << 12)) return 0;
+  const int lg = 63 - __builtin_clzll(n);  // floor(log2 n)
+  return std::min(20, lg - 2);
 }
 
 __global__ void tile_count_kernel(const uint8_t* __restrict__ keep, uint64_t n, uint64_t* __restrict__ counts) {
@@ -633,11 +669,13 @@ cudaError_t cut_leaves_device(uint64_t n, uint64_t* src, uint64_t* dst, uint64_t
   if ((e = cudaMemsetAsync(indeg, 0, n * sizeof(unsigned int), st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(alive, 1, n, st)) != cudaSuccess) return e;
   check_sorted_kernel<<<grid_for(n), kT, 0, st>>>(src, n, err);
-  resolve_kernel<<<grid_for(n), kT, 0, st>>>(src, n, dst, idx);
+  const int dbits = dir_bits(n);  // the directory lives in f1 until the passes start
+  if (dbits) dir_build_kernel<<<grid_for(n), kT, 0, st>>>(src, n, dbits, f1);
+  resolve_kernel<<<grid_for(n), kT, 0, st>>>(src, n, dst, idx, dbits, f1);
   indeg_count_kernel<<<grid_for(n), kT, 0, st>>>(idx, n, indeg);
   frontier_init_kernel<<<grid_for(n), kT, 0, st>>>(indeg, n, f0, &ctl->cnt[0]);
   sum_kernel<<<std::min(grid_for(n), 4096u), kT, 0, st>>>(size, n, &ctl->sum);
-  *launches += 5;
+  *launches += dbits ? 6 : 5;
   const unsigned long long alive0 = n;
   if ((e = cudaMemcpyAsync(&ctl->alive, &alive0, 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) return e;
   unsigned int herr = 0;
@@ -864,7 +902,7 @@ cudaError_t count_cycles_device(uint64_t n, const uint64_t* src, const uint64_t*
   if ((e = cudaMemsetAsync(err, 0, 16, st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(indeg, 0, n * sizeof(unsigned int), st)) != cudaSuccess) return e;
   check_sorted_kernel<<<grid_for(n), kT, 0, st>>>(src, n, err);
-  resolve_kernel<<<grid_for(n), kT, 0, st>>>(src, n, dst, idx);
+  resolve_kernel<<<grid_for(n), kT, 0, st>>>(src, n, dst, idx, 0, nullptr);
   indeg_kernel<<<grid_for(n), kT, 0, st>>>(idx, n, indeg, err);
   perm_check_kernel<<<grid_for(n), kT, 0, st>>>(indeg, n, err);
   *launches += 4;
