@@ -292,14 +292,13 @@ def _gathered_tail(ex, shard, passes, alive: int):
         raise ValueError(f"a removed leaf's destination has no surviving record; input was not closed ({e})") from e
     passes.extend(tail)
     # the gathered survivors stay in source order: this rank's are the run between its own
-    # first and last alive source (unsigned order: compared with the sign bit flipped)
+    # first and last alive source (located on the host: the fixpoint set is small)
     if not n_loc or not n_fix:
         return 0, passes
-    flip = torch.iinfo(torch.int64).min
-    surv = g[0][:n_fix] ^ flip
-    ends = torch.stack([cols[0][0], cols[0][n_loc - 1]]) ^ flip
-    a = int(torch.searchsorted(surv, ends[:1]).item())
-    b = int(torch.searchsorted(surv, ends[1:], right=True).item())
+    surv = g[0][:n_fix].cpu().numpy().view(np.uint64)
+    ends = cols[0][[0, n_loc - 1]].cpu().numpy().view(np.uint64)
+    a = int(np.searchsorted(surv, ends[0], side="left"))
+    b = int(np.searchsorted(surv, ends[1], side="right"))
     for k in range(5):
         cols[k][: b - a] = g[k][a:b]
     return b - a, passes
