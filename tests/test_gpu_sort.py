@@ -86,3 +86,32 @@ def test_device_sort_out_of_place(gpu, lc):
     bad = (C.c_void_p * 5)(*[t.data_ptr() for t in d_out], d_out[0].data_ptr(), None)
     with pytest.raises(N.NativeError):
         N.check(N.lib.lc_sort_edges_device(ctx.handle, n, pin, bad, None))
+
+
+def test_device_sort_unaligned_columns(gpu, lc):
+    """Key columns 8 bytes past a 16-byte boundary (a view one element into a buffer):
+    the window histogram and the group-bounds kernel take their one-key-per-load paths."""
+    import torch
+
+    from paper_1210_6411_b200 import _native as N
+
+    ctx = N.context()
+    dev = torch.device("cuda", ctx.device)
+    rng = np.random.default_rng(5)
+    n = (1 << 18) + 3
+    cols = [_keys("a51", n, rng), rng.integers(0, 1 << 62, size=n, dtype=np.uint64), np.arange(n, dtype=np.uint64)]
+    bufs_in = [torch.empty(n + 1, dtype=torch.int64, device=dev) for _ in cols]
+    bufs_out = [torch.empty(n + 1, dtype=torch.int64, device=dev) for _ in cols]
+    d_in = [b[1:] for b in bufs_in]
+    d_out = [b[1:] for b in bufs_out]
+    for t, c in zip(d_in, cols):
+        t.copy_(torch.from_numpy(c.view(np.int64)))
+    assert all(t.data_ptr() % 16 == 8 for t in d_in + d_out)
+    pin = (C.c_void_p * 5)(*[t.data_ptr() for t in d_in], None, None)
+    pout = (C.c_void_p * 5)(*[t.data_ptr() for t in d_out], None, None)
+    torch.cuda.synchronize()
+    N.check(N.lib.lc_sort_edges_device(ctx.handle, n, pin, pout, None))
+    torch.cuda.synchronize()
+    order = np.argsort(cols[0], kind="stable")
+    for c, o in zip(cols, d_out):
+        assert (o.cpu().numpy().view(np.uint64) == c[order]).all()
