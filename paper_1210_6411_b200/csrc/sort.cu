@@ -11,7 +11,7 @@
 //     the fixed value -- or an already sorted input; their pass kernels return at once)
 //     and assigns the ping-pong buffers backwards from the last pass that runs, so the
 //     whole sort is enqueued without a host round trip;
-//   * a pass kernel takes tiles of 2560 keys in launch order (an atomic ticket, so a
+//   * a pass kernel takes tiles of 2816 keys in launch order (an atomic ticket, so a
 //     tile's predecessors are always resident): it loads the tile's keys into registers
 //     and its row payload into shared memory (cp.async, overlapping the ranking), ranks
 //     each key within its warp (match on the digit, warp-private counters), publishes
@@ -45,13 +45,13 @@ constexpr uint32_t kFullMask = 0xffffffffu;
 constexpr int kSortThreads = LC_SORT_THREADS;  // a multiple of 256 (threads 0..255 own a digit each)
 constexpr int kSortWarps = kSortThreads / 32;
 #ifndef LC_SORT_ITEMS
-#define LC_SORT_ITEMS 10
+#define LC_SORT_ITEMS 11
 #endif
 #ifndef LC_SORT_MINBLOCKS
 #define LC_SORT_MINBLOCKS 4
 #endif
 constexpr int kItems = LC_SORT_ITEMS;               // keys per thread
-constexpr int kTileKeys = kSortThreads * kItems;    // 2560 (4 blocks per SM)
+constexpr int kTileKeys = kSortThreads * kItems;    // 2816 (4 blocks per SM: 56 KB each)
 constexpr int kBins = 256;
 constexpr int kBytes = 8;
 constexpr int kCols = 5;
