@@ -273,6 +273,24 @@ __global__ void cut_pass_end_kernel(CutCtl* ctl, int w, uint64_t* __restrict__ p
 // them by atomics, which the L1 would not see.  A frontier entry carries its record's
 // destination, loaded while the pass that made it a leaf waits on its in-degree atomic,
 // so a pass's dependent chain is one L2 atomic round trip rather than a load and then one.
+// the next hop's lines into L2 while this pass waits on its atomics: the new leaf j's
+// destination jj is folded into (and its in-degree dropped) in the next pass
+#ifndef LC_CUT_TAIL_PREFETCH
+#define LC_CUT_TAIL_PREFETCH 1
+#endif
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void prefetch_hop(uint64_t jj, const uint64_t* idx, const unsigned long long* size,
+                                             const unsigned long long* depth, const unsigned int* indeg) {
+#if LC_CUT_TAIL_PREFETCH
+  if (jj != kNone) {
+    prefetch_l2(indeg + jj);
+    prefetch_l2(size + jj);
+    prefetch_l2(depth + jj);
+    prefetch_l2(idx + jj);
+  }
+#endif
+}
+
 constexpr int kTailThreads = 1024;
 constexpr uint32_t kTailMax = 6144;  // frontier entries per buffer (2 x 96 KB of shared memory)
 constexpr size_t kTailSmem = 2 * kTailMax * sizeof(ulonglong2);
@@ -342,7 +360,10 @@ __global__ void __launch_bounds__(kTailThreads) cut_tail_kernel(CutCtl* ctl, uin
         const bool leaf = atomicSub(&indeg[j], 1u) == 1u;
         atomicAdd(&size[j], __ldcg(&size[i]) + 1ull);
         atomicMax(&depth[j], __ldcg(&depth[i]) + 1ull);
-        if (leaf) fn[atomicAdd(cnext, 1u)] = make_ulonglong2(j, jj);
+        if (leaf) {
+          prefetch_hop(jj, idx, size, depth, indeg);
+          fn[atomicAdd(cnext, 1u)] = make_ulonglong2(j, jj);
+        }
       }
     }
     if (tid == 0) {
@@ -377,6 +398,7 @@ __global__ void __launch_bounds__(kTailThreads) cut_tail_kernel(CutCtl* ctl, uin
           push = atomicSub(&indeg[j], 1u) == 1u;
           atomicAdd(&size[j], __ldcg(&size[i]) + 1ull);
           atomicMax(&depth[j], __ldcg(&depth[i]) + 1ull);
+          if (push) prefetch_hop(jj, idx, size, depth, indeg);
         }
       }
       const uint32_t pushed = __ballot_sync(0xffffffffu, push);
