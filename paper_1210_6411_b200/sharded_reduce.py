@@ -230,12 +230,12 @@ def cut_leaves_sharded(src, dst, dist, subtree_size, subtree_depth, *, max_passe
             shard.close()
         raise ValueError(f"sharded leaf cutting: {failure or 'another rank rejected its shard'}")
     try:
-        return _drive(ex, shard, int(count.sum()), max_passes)
+        return _drive(ex, shard, cols, int(count.sum()), max_passes)
     finally:
         shard.close()
 
 
-def _drive(ex, shard, total: int, max_passes: int):
+def _drive(ex, shard, cols, total: int, max_passes: int):
     W = ex.world
     # phase 0: in-degrees
     send, counts, _, err = shard.emit(0)
@@ -262,7 +262,7 @@ def _drive(ex, shard, total: int, max_passes: int):
             break
         if (not max_passes and getattr(shard, "gathers_tail", False) and removed <= TAIL_LEAVES
                 and 0 < alive <= TAIL_ALIVE and os.environ.get("LFSR_SHARD_TAIL", "1") != "0"):
-            return _gathered_tail(ex, shard, passes, alive)
+            return _gathered_tail(ex, shard, cols, passes, alive)
     n_out, rc = shard.finish()
     flags = ex.allgather([rc])
     if flags.any():
@@ -270,7 +270,7 @@ def _drive(ex, shard, total: int, max_passes: int):
     return n_out, passes
 
 
-def _gathered_tail(ex, shard, passes, alive: int):
+def _gathered_tail(ex, shard, cols, passes, alive: int):
     """Finish the cut on the all-gathered alive records (module docstring, "The tail")."""
     import torch
 
@@ -283,7 +283,6 @@ def _gathered_tail(ex, shard, passes, alive: int):
     counts = mat[:, 1]
     if int(counts.sum()) != alive:
         raise RuntimeError(f"sharded leaf cutting: {int(counts.sum())} alive records gathered, {alive} expected")
-    cols = shard.cols
     rows = ex.allgather_rows(torch.stack([c[:n_loc] for c in cols], 1), counts)
     g = [rows[:, k].contiguous() for k in range(5)]
     try:

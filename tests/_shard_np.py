@@ -11,6 +11,8 @@ LC_ERR_NOT_CLOSED = -8
 
 
 class NumpyShard:
+    gathers_tail = False  # NumpyShardTail: let the driver finish on the gathered records
+
     def __init__(self, cols, n_ranks, rank_first, rank_count):
         self.cols = [c.numpy().view(np.uint64) for c in cols]  # shares memory with the tensors
         self.src, self.dst, _, self.size, self.depth = self.cols
@@ -74,3 +76,19 @@ class NumpyShard:
 
     def close(self):
         pass
+
+
+class NumpyShardTail(NumpyShard):
+    gathers_tail = True
+
+
+def numpy_cut_leaves_tensors(src, dst, dist, subtree_size, subtree_depth, *, max_passes=0):
+    """Stand-in for reduce.cut_leaves_tensors on CPU tensors (the reduce oracle, in place)."""
+    from oracle import reduce_np
+
+    cols = [t.numpy().view(np.uint64) for t in (src, dst, dist, subtree_size, subtree_depth)]
+    res = reduce_np.cut_leaves(*cols, max_passes=max_passes)
+    n = res[0].size
+    for c, r in zip(cols, res[:5]):
+        c[:n] = r
+    return n, [tuple(int(v) for v in p) for p in res[5]]

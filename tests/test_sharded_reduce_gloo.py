@@ -1,7 +1,8 @@
 """Multi-rank leaf cutting (sharded_reduce.py) under gloo on CPU: world sizes 2 and 3,
 contiguous source-range shards (one empty), the per-pass all-gather / all-to-all
 protocol of the multi-GPU path.  Per-rank shard kernels are replaced by the test-only
-numpy stand-in (tests/_shard_np.py); the GPU form of the same driver runs in
+numpy stand-in (tests/_shard_np.py), with and without the gathered tail (whose
+single-GPU cut is the reduce oracle here); the GPU form of the same driver runs in
 tests/test_gpu_sharded_reduce.py.  Results must equal the reduce oracle (pinned to the
 reference's cut_leaves_pass, tests/test_oracle.py)."""
 
@@ -61,19 +62,22 @@ def _worker(rank, world, port, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from _shard_np import NumpyShard
+        from _shard_np import NumpyShard, NumpyShardTail, numpy_cut_leaves_tensors
+        from paper_1210_6411_b200 import reduce as R
         from paper_1210_6411_b200.sharded_reduce import cut_leaves_sharded
 
-        for name, (cols, max_passes, mode) in _cases().items():
-            n = cols[0].size
-            lo, hi = _split(n, rank, world, mode)
-            t = [torch.from_numpy(c[lo:hi].copy().view(np.int64)) for c in cols]
-            try:
-                n_out, passes = cut_leaves_sharded(*t, max_passes=max_passes, shard_factory=NumpyShard)
-                rows = np.stack([c[:n_out].numpy().view(np.uint64) for c in t], 1).tolist()
-                out[(name, rank)] = ("ok", rows, passes)
-            except ValueError as e:
-                out[(name, rank)] = ("ValueError", str(e), None)
+        R.cut_leaves_tensors = numpy_cut_leaves_tensors  # the gathered tail's single-GPU cut, on CPU
+        for tail, factory in ((False, NumpyShard), (True, NumpyShardTail)):
+            for name, (cols, max_passes, mode) in _cases().items():
+                n = cols[0].size
+                lo, hi = _split(n, rank, world, mode)
+                t = [torch.from_numpy(c[lo:hi].copy().view(np.int64)) for c in cols]
+                try:
+                    n_out, passes = cut_leaves_sharded(*t, max_passes=max_passes, shard_factory=factory)
+                    rows = np.stack([c[:n_out].numpy().view(np.uint64) for c in t], 1).tolist()
+                    out[(name, tail, rank)] = ("ok", rows, passes)
+                except ValueError as e:
+                    out[(name, tail, rank)] = ("ValueError", str(e), None)
     finally:
         dist.destroy_process_group()
 
@@ -89,8 +93,8 @@ def _run(world):
 def _check(out, world):
     from oracle import reduce_np
 
-    for name, (cols, max_passes, _) in _cases().items():
-        res = [out[(name, r)] for r in range(world)]
+    for (name, (cols, max_passes, _)), tail in ((c, t) for c in _cases().items() for t in (False, True)):
+        res = [out[(name, tail, r)] for r in range(world)]
         if name == "broken":
             assert all(r[0] == "ValueError" for r in res), res
             continue
